@@ -1,0 +1,331 @@
+"""Benchmark: CKKS rotation key-switches/s at N=2^16, L=24, dnum=3 (BASELINE config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the BASELINE C3 workload on each GPU: 64 independent rotation
+key-switches (distinct ciphertexts, keys and Galois elements 5^k), batched
+through ck_rotate (C ABI).  Inputs are generated on the device (counter-based
+generator, bit-identical to the host generator the oracle uses) and exceed L2
+(8 GB per step), so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun): every rank processes its own 64 units (weak scaling,
+no data-path collective); time = max over ranks of CUDA-event time.
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy port in oracle/, the only CPU form of the reference that can run on
+the GPU box) on all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "key-switches/sec at N=2^16,L=24,dnum=3; achieved HBM GB/s vs B200 peak"
+UNIT = "key-switches/s"
+SEED = 20211212
+CPU_WORKERS_MAX = 32
+
+
+def _peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ks_bytes(params, limbs=None) -> int:
+    """Compulsory HBM bytes per rotation key-switch:
+    8 N (l [a] + l [b] + 2 beta (l+K) [evk a,b rows] + 2 l [out])."""
+    l = params.limbs if limbs is None else limbs
+    beta = len(params.digit_spans(l))
+    K = len(params.special)
+    return 8 * params.n_ring * (l + l + 2 * beta * (l + K) + 2 * l)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.QUERY}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except Exception:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- CPU oracle
+def _cpu_task(args):
+    unit, k = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import ckks_np
+    from paper_2112_06396_b200 import synth
+    from paper_2112_06396_b200.digest import digest
+    from paper_2112_06396_b200.params import config
+    p = config("C3").params
+    a, b, kb, ka = synth.rotation_inputs(p, SEED, unit)
+    t0 = time.perf_counter()
+    oa, ob = ckks_np.rotate_galois(p, a, b, kb, ka, pow(5, k, 2 * p.n_ring))
+    return unit, time.perf_counter() - t0, digest(oa, ob)
+
+
+def _warm(_):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import ckks_np
+    from paper_2112_06396_b200.params import config
+    p = config("C3").params
+    for q in p.full_moduli:
+        ckks_np.twiddles(q, p.n_ring)
+    return True
+
+
+def _init_worker():
+    os.environ["OMP_NUM_THREADS"] = "1"
+
+
+def cpu_pool(wait: bool = True):
+    """Fork the CPU workers BEFORE CUDA is initialised in this process."""
+    workers = max(1, min(os.cpu_count() or 1, CPU_WORKERS_MAX))
+    ctx = mp.get_context("fork")
+    pool = ctx.Pool(workers, initializer=_init_worker)
+    warm = pool.map_async(_warm, range(workers))
+    if wait:
+        warm.wait()
+    return pool, workers
+
+
+def cpu_sample(pool, workers, units, ks):
+    t0 = time.perf_counter()
+    res = pool.map(_cpu_task, list(zip(units, ks)), chunksize=1)
+    wall = time.perf_counter() - t0
+    return wall, res
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    from paper_2112_06396_b200.params import config, galois_exponents
+    p = config("C3").params
+    allk = galois_exponents(p.n_ring, 64, SEED)
+    pool, workers = cpu_pool()
+    units = list(range(workers))
+    ks = [allk[u % 64] for u in units]
+    for _ in range(args.warmup):
+        cpu_sample(pool, workers, units[:1], ks[:1])
+    times = []
+    for _ in range(args.steps):
+        wall, _ = cpu_sample(pool, workers, units, ks)
+        times.append(wall)
+    pool.close()
+    total = sum(times)
+    value = workers * args.steps / total
+    sample = f"{workers} C3 rotation key-switches per step (one per worker process), numpy port of the reference (oracle/ckks_np.py)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded counter-based residues)",
+        "config": {"workload": "C3: 64 independent rotation key-switches, N=2^16, L=24x54b, dnum=3, K=8x60b"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_06396_b200 import _lib
+    from paper_2112_06396_b200.digest import digest
+    from paper_2112_06396_b200.params import config, galois_exponents
+    from paper_2112_06396_b200.workload import RotationBatch
+
+    pool = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        pool, workers = cpu_pool(wait=False)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lib = _lib.load()
+    wl = config("C3")
+    p = wl.params
+    B = args.batch
+    units = [rank * B + i for i in range(B)]
+    allk = galois_exponents(p.n_ring, B * world, SEED)
+    ks = [allk[u] for u in units]
+    wb = RotationBatch(p, SEED, units, ks=ks)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        wb.run()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    n0 = lib.ck_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        wb.run()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.ck_launch_count() - n0
+    barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms / args.steps
+    value = B * world * args.steps / (ms / 1000.0)
+
+    # ---- roofline of the key-switch (per GPU)
+    peak, peak_kind = _peaks()
+    bytes_ks = ks_bytes(p)
+    achieved = bytes_ks * B / (ms_step / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": args.traffic,
+                "kernel": "ck_rotate pipeline (batched key-switch, all launches of one step)",
+                "algorithmic_bytes_per_unit": bytes_ks, "units_per_launch": B,
+                "peak_kind": peak_kind}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        ins = [wb.a, wb.b, wb.key_b, wb.key_a]
+        host_in = [t.cpu().pin_memory() for t in ins]
+        host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64).pin_memory() for _ in range(2)]
+        ke = max(1, min(args.steps, args.e2e_steps))
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            for d, h in zip(ins, host_in):
+                d.copy_(h, non_blocking=True)
+            wb.run()
+            host_out[0].copy_(wb.out_a, non_blocking=True)
+            host_out[1].copy_(wb.out_b, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": B * world * ke / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": wb.input_bytes(), "d2h_bytes_per_step": wb.output_bytes(),
+               "steps": ke, "note": "ciphertexts AND per-rotation evaluation keys copied H2D every step"}
+
+    # ---- CPU baseline (oracle port on host cores), rank 0 at N=1
+    cpu = None
+    if pool is not None:
+        n_s = min(workers, B)
+        wall, res = cpu_sample(pool, workers, units[:n_s], ks[:n_s])
+        pool.close()
+        torch.cuda.synchronize()
+        parity = all(dg == digest(wb.out_a[i].cpu().numpy(), wb.out_b[i].cpu().numpy())
+                     for i, (_, _, dg) in enumerate(res))
+        cpu = {"value": n_s / wall, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"{n_s} of the {B} C3 rotations, one per worker process (numpy port, oracle/ckks_np.py)",
+               "parity_vs_gpu_bit_exact": parity}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded counter-based residues, generated on device)",
+            "config": {"workload": wl.desc, "units_per_gpu_per_step": B,
+                       "global_units_per_step": B * world, "limbs": p.limbs,
+                       "special": len(p.special), "dnum": p.dnum, "log_n": p.logn,
+                       "l2": "inputs larger than L2 (8 GB/step/GPU), no flush",
+                       "parallelism": f"batch-partitioned x{world}"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per unit (from profiles/), reported as roofline.traffic")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,433 @@
+"""GPU mirror of the reference key-switching API (ckkslab/ckks.py:359-740).
+
+Same function names and argument meaning as the reference: ``hrotate``,
+``rotate``, ``conjugate``, ``mult``, ``new_mult``, ``pt_matvec``,
+``raise_modulus`` and the internals ``_decomp_modup``, ``_kskip``,
+``_moddown_poly``, ``_moddown_pair``, ``pmodup``, ``_ntt_rows``,
+``_rescale_poly``; plus ``bsgs`` (the hoisted BSGS linear transform of
+SURVEY 8(a) a19) and batched entry points (``rotate_batch``) used by the
+benchmark.  Polynomials are RnsPoly with torch.uint64 CUDA data; all compute
+runs in libckks_b200.so (no CPU fallback).
+
+Reference conventions kept (SURVEY section 0 traps):
+  * rotate(ct, r) uses Galois element 5^(-r) mod 2N (ckks.py:662);
+  * hrotate/rotate: ModUp first, then automorph of the digits (hoisted order);
+    conjugate: automorph first, then ModUp (ckks.py:677-678);
+  * merged ModDown drops (q_last,) + specials in that order (ckks.py:646-650).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+from .device import plan_for, ptr, shoup_pairs, stream_handle, to_dev
+from .params import CkksParams  # noqa: F401  (re-export, mirrors ckks.CkksParams)
+from .rnspoly import RnsPoly, automorph_rows, ntt_rows
+
+# ------------------------------------------------------------------ types
+
+
+@dataclass
+class SwitchingKey:
+    """ckks.SwitchingKey (ckks.py:188-225); expanded keys only on the device.
+
+    b, a: (dnum, L+K, N) full-basis rows.  A compressed key (seed, a=None) is
+    expanded on the host with the reference's SHAKE256 XOF before upload
+    (on-device expansion is the next item in SURVEY 8(f)).
+    """
+
+    moduli: tuple[int, ...]
+    b: torch.Tensor
+    seed: bytes | None = None
+    a: torch.Tensor | None = None
+
+    def __post_init__(self):
+        self.b = to_dev(self.b)
+        if self.a is None:
+            assert self.seed is not None
+            self.a = to_dev(_expand_a(self.seed, self.moduli, tuple(self.b.shape)))
+        else:
+            self.a = to_dev(self.a)
+
+    @property
+    def compressed(self) -> bool:
+        return False
+
+
+def _xof_uniform(seed: bytes, label: bytes, q: int, n: int) -> np.ndarray:
+    """Restatement of ckks._xof_uniform (ckks.py:169-185): SHAKE256 stream,
+    rejection of words >= floor(2^64/q)*q, then % q; host-side key expansion."""
+    import hashlib
+    bound = np.uint64((1 << 64) // q * q)
+    out = np.empty(n, dtype=np.uint64)
+    have, offset = 0, 0
+    length = 8 * (n + n // 8 + 16)
+    xof = hashlib.shake_256(seed + label)
+    while have < n:
+        raw = np.frombuffer(xof.digest(offset + length)[offset:], dtype="<u8")
+        offset += length
+        keep = raw[raw < bound]
+        take = min(n - have, keep.size)
+        out[have:have + take] = keep[:take] % np.uint64(q)
+        have += take
+        length = 8 * (n - have + 16)
+    return out
+
+
+def _expand_a(seed: bytes, moduli, shape) -> np.ndarray:
+    dn, lm, n = shape
+    a = np.empty(shape, dtype=np.uint64)
+    for j in range(dn):
+        for i in range(lm):
+            a[j, i] = _xof_uniform(seed, b"ksk%d:%d" % (j, i), moduli[i], n)
+    return a
+
+
+@dataclass
+class KeySet:
+    params: CkksParams
+    s: RnsPoly | None
+    relin: SwitchingKey | None
+    rot: dict = field(default_factory=dict)
+    conj: SwitchingKey | None = None
+
+
+@dataclass
+class Ciphertext:
+    a: RnsPoly
+    b: RnsPoly
+    delta: float
+
+    @property
+    def limbs(self) -> int:
+        return len(self.a.moduli)
+
+    def copy(self) -> "Ciphertext":
+        return Ciphertext(self.a.copy(), self.b.copy(), self.delta)
+
+
+def _L():
+    return _lib.load()
+
+
+# ------------------------------------------------------------- internals
+
+def _ntt_rows(data, moduli, n: int, inverse: bool) -> torch.Tensor:
+    return ntt_rows(to_dev(data), tuple(moduli), inverse)
+
+
+def _galois(params: CkksParams, r: int) -> int:
+    return pow(5, -r, 2 * params.n_ring)
+
+
+def _decomp_modup_raw(params: CkksParams, a: torch.Tensor, limbs: int) -> torch.Tensor:
+    """ck_modup -> (beta, l+K, N) digits tensor."""
+    plan = plan_for(params)
+    beta = len(params.digit_spans(limbs))
+    R = limbs + len(params.special)
+    dig = torch.empty((beta, R, params.n_ring), dtype=torch.uint64, device="cuda")
+    ws = plan.workspace(limbs, 1)
+    check(_L().ck_modup(plan.h, ptr(a), limbs, ptr(dig), ptr(ws), 1, stream_handle()), "ck_modup")
+    return dig
+
+
+def _decomp_modup(params: CkksParams, a: RnsPoly) -> list[RnsPoly]:
+    """ckks._decomp_modup (ckks.py:421-441)."""
+    limbs = len(a.moduli)
+    assert a.moduli == params.chain[:limbs] and a.rep == "eval"
+    dig = _decomp_modup_raw(params, a.data, limbs)
+    raised = params.raised_moduli(limbs)
+    return [RnsPoly(raised, dig[j], "eval") for j in range(dig.shape[0])]
+
+
+def _stack_digits(digits) -> torch.Tensor:
+    if isinstance(digits, torch.Tensor):
+        return digits
+    return torch.stack([d.data for d in digits]).contiguous()
+
+
+def _kskip_raw(params, dig: torch.Tensor, key: SwitchingKey, limbs: int, t: int = 1):
+    plan = plan_for(params)
+    R = limbs + len(params.special)
+    u = torch.empty((R, params.n_ring), dtype=torch.uint64, device="cuda")
+    v = torch.empty_like(u)
+    check(_L().ck_kskip(plan.h, ptr(dig), ptr(key.b), ptr(key.a), limbs, t % (2 * params.n_ring),
+                        None, ptr(u), ptr(v), 1, stream_handle()), "ck_kskip")
+    return u, v
+
+
+def _kskip(params: CkksParams, digits, key: SwitchingKey) -> tuple[RnsPoly, RnsPoly]:
+    """ckks._kskip (ckks.py:450-465)."""
+    raised = digits[0].moduli
+    limbs = len(raised) - len(params.special)
+    u, v = _kskip_raw(params, _stack_digits(digits), key, limbs)
+    return RnsPoly(raised, u, "eval"), RnsPoly(raised, v, "eval")
+
+
+def _moddown_raw(params, x: torch.Tensor, limbs: int, merged: int,
+                 addend: torch.Tensor | None = None, t: int = 1) -> torch.Tensor:
+    plan = plan_for(params)
+    keep = limbs if merged == 0 else limbs - 1
+    out = torch.empty((keep, params.n_ring), dtype=torch.uint64, device="cuda")
+    xs = x.clone()  # ck_moddown clobbers the dropped rows; reference is pure
+    ws = plan.workspace(limbs, 1)
+    check(_L().ck_moddown(plan.h, ptr(xs), limbs, merged, ptr(out), ptr(addend),
+                          t % (2 * params.n_ring), ptr(ws), 1, stream_handle()), "ck_moddown")
+    return out
+
+
+def _moddown_pair(params: CkksParams, u: RnsPoly, v: RnsPoly, keep_limbs: int):
+    """ckks._moddown_pair (ckks.py:468-475)."""
+    assert u.moduli == params.raised_moduli(keep_limbs)
+    keep = u.moduli[:keep_limbs]
+    return (RnsPoly(keep, _moddown_raw(params, u.data, keep_limbs, 0), "eval"),
+            RnsPoly(keep, _moddown_raw(params, v.data, keep_limbs, 0), "eval"))
+
+
+def _moddown_merged(params: CkksParams, x: RnsPoly, limbs: int) -> RnsPoly:
+    """ModDown by P*q_last (ckks.py:643-651, 712-717)."""
+    return RnsPoly(x.moduli[:limbs - 1], _moddown_raw(params, x.data, limbs, 1), "eval")
+
+
+def _rescale_poly_p(params: CkksParams, x: RnsPoly) -> RnsPoly:
+    """ckks._rescale_poly (ckks.py:375-394) inside a plan's chain."""
+    limbs = len(x.moduli)
+    return RnsPoly(x.moduli[:-1], _moddown_raw(params, x.data, limbs, 2), "eval")
+
+
+def pmodup(params: CkksParams, x: RnsPoly) -> RnsPoly:
+    """ckks.pmodup (ckks.py:478-489)."""
+    mods = x.moduli
+    raised = params.raised_moduli(len(mods))
+    big_p = 1
+    for p in params.special:
+        big_p *= p
+    data = torch.zeros((len(raised), x.n), dtype=torch.uint64, device="cuda")
+    data[:len(mods)] = x.mul_scalars([big_p % q for q in mods]).data
+    return RnsPoly(raised, data, "eval")
+
+
+# ------------------------------------------------------------ public API
+
+def add(ct1: Ciphertext, ct2: Ciphertext) -> Ciphertext:
+    assert abs(ct1.delta / ct2.delta - 1) < 2e-6
+    return Ciphertext(ct1.a.add(ct2.a), ct1.b.add(ct2.b), ct1.delta)
+
+
+def sub(ct1: Ciphertext, ct2: Ciphertext) -> Ciphertext:
+    assert abs(ct1.delta / ct2.delta - 1) < 2e-6
+    return Ciphertext(ct1.a.sub(ct2.a), ct1.b.sub(ct2.b), ct1.delta)
+
+
+def negate(ct: Ciphertext) -> Ciphertext:
+    return Ciphertext(ct.a.neg(), ct.b.neg(), ct.delta)
+
+
+def drop_limbs(ct: Ciphertext, limbs: int) -> Ciphertext:
+    assert limbs <= ct.limbs
+    mods = ct.a.moduli[:limbs]
+    return Ciphertext(RnsPoly(mods, ct.a.data[:limbs].clone(), "eval"),
+                      RnsPoly(mods, ct.b.data[:limbs].clone(), "eval"), ct.delta)
+
+
+def rescale(params: CkksParams, ct: Ciphertext) -> Ciphertext:
+    q_last = ct.a.moduli[-1]
+    return Ciphertext(_rescale_poly_p(params, ct.a), _rescale_poly_p(params, ct.b),
+                      ct.delta / q_last)
+
+
+def _tensor(ct1: Ciphertext, ct2: Ciphertext):
+    a3 = ct1.a.mul(ct2.a)
+    b3 = ct1.a.mul(ct2.b).add(ct2.a.mul(ct1.b))
+    c3 = ct1.b.mul(ct2.b)
+    return a3, b3, c3
+
+
+def mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext) -> Ciphertext:
+    """ckks.mult (ckks.py:591-600): tensor, relinearise, rescale."""
+    a3, b3, c3 = _tensor(ct1, ct2)
+    digits = _decomp_modup(params, a3)
+    u_hat, v_hat = _kskip(params, digits, keys.relin)
+    u, v = _moddown_pair(params, u_hat, v_hat, len(a3.moduli))
+    out = Ciphertext(b3.add(u), c3.add(v), ct1.delta * ct2.delta)
+    return rescale(params, out)
+
+
+def _const_poly(moduli, n: int, integer: int) -> RnsPoly:
+    """encode_const (ckks.py:530-537): NTT of a degree-0 poly = constant in every slot."""
+    vals = np.array([integer % q for q in moduli], dtype=np.uint64)
+    return RnsPoly(moduli, np.repeat(vals[:, None], n, axis=1), "eval")
+
+
+def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext, *,
+             value_mult: int = 1, const: float = 0.0, addend: Ciphertext | None = None,
+             addend_sign: int = 1) -> Ciphertext:
+    """ckks.new_mult (ckks.py:603-652): relin ModDown merged with the rescale."""
+    lim = min(ct1.limbs, ct2.limbs)
+    ct1, ct2 = drop_limbs(ct1, lim), drop_limbs(ct2, lim)
+    a3, b3, c3 = _tensor(ct1, ct2)
+    if value_mult != 1:
+        scal = [value_mult % q for q in a3.moduli]
+        a3, b3, c3 = a3.mul_scalars(scal), b3.mul_scalars(scal), c3.mul_scalars(scal)
+    prod_delta = ct1.delta * ct2.delta
+    if addend is not None:
+        assert addend.limbs >= lim
+        ad = drop_limbs(addend, lim)
+        ratio = prod_delta / ad.delta
+        assert ratio > 2.0 ** 40
+        lift = addend_sign * round(ratio)
+        scal = [lift % q for q in ad.a.moduli]
+        b3 = b3.add(ad.a.mul_scalars(scal))
+        c3 = c3.add(ad.b.mul_scalars(scal))
+    if const:
+        c3 = c3.add(_const_poly(c3.moduli, params.n_ring, round(const * prod_delta)))
+    digits = _decomp_modup(params, a3)
+    u_hat, v_hat = _kskip(params, digits, keys.relin)
+    u_hat = u_hat.add(pmodup(params, b3))
+    v_hat = v_hat.add(pmodup(params, c3))
+    a_out = _moddown_merged(params, u_hat, lim)
+    b_out = _moddown_merged(params, v_hat, lim)
+    return Ciphertext(a_out, b_out, prod_delta / u_hat.moduli[lim - 1])
+
+
+def hrotate(params: CkksParams, keys: KeySet, ct: Ciphertext, rotations) -> list[Ciphertext]:
+    """ckks.hrotate (ckks.py:655-667): one shared ModUp, per-rotation KSKIP+ModDown."""
+    limbs = ct.limbs
+    assert ct.a.moduli == params.chain[:limbs]
+    dig = _decomp_modup_raw(params, ct.a.data, limbs)
+    outs = []
+    for r in rotations:
+        t = _galois(params, r)
+        key = keys.rot[r]  # KeyError like the reference (ckks.py:664)
+        u, v = _kskip_raw(params, dig, key, limbs, t)
+        a_out = _moddown_raw(params, u, limbs, 0)
+        b_out = _moddown_raw(params, v, limbs, 0, addend=ct.b.data, t=t)
+        mods = ct.a.moduli
+        outs.append(Ciphertext(RnsPoly(mods, a_out, "eval"), RnsPoly(mods, b_out, "eval"), ct.delta))
+    return outs
+
+
+def _rotate_raw(params, a, b, key: SwitchingKey, t: int, mode: int, limbs: int):
+    plan = plan_for(params)
+    out_a = torch.empty_like(a)
+    out_b = torch.empty_like(b)
+    ws = plan.workspace(limbs, 1)
+    check(_L().ck_rotate(plan.h, ptr(a), ptr(b), ptr(key.b), ptr(key.a), limbs,
+                         t % (2 * params.n_ring), None, mode, ptr(out_a), ptr(out_b), ptr(ws), 1,
+                         stream_handle()), "ck_rotate")
+    return out_a, out_b
+
+
+def rotate(params: CkksParams, keys: KeySet, ct: Ciphertext, r: int) -> Ciphertext:
+    """ckks.rotate (ckks.py:670-671) == hrotate(ct, (r,))[0], one fused C call."""
+    key = keys.rot[r]
+    a, b = _rotate_raw(params, ct.a.data, ct.b.data, key, _galois(params, r), 0, ct.limbs)
+    return Ciphertext(RnsPoly(ct.a.moduli, a, "eval"), RnsPoly(ct.b.moduli, b, "eval"), ct.delta)
+
+
+def conjugate(params: CkksParams, keys: KeySet, ct: Ciphertext) -> Ciphertext:
+    """ckks.conjugate (ckks.py:674-681): automorph first, then ModUp."""
+    key = keys.conj
+    assert key is not None
+    a, b = _rotate_raw(params, ct.a.data, ct.b.data, key, 2 * params.n_ring - 1, 1, ct.limbs)
+    return Ciphertext(RnsPoly(ct.a.moduli, a, "eval"), RnsPoly(ct.b.moduli, b, "eval"), ct.delta)
+
+
+def pt_matvec(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict,
+              diag_delta: float) -> Ciphertext:
+    """ckks.pt_matvec (ckks.py:684-719), double-hoisted."""
+    limbs = ct.limbs
+    raised = params.raised_moduli(limbs)
+    dig = _decomp_modup_raw(params, ct.a.data, limbs)
+    acc_u = RnsPoly.zeros(raised, params.n_ring, "eval")
+    acc_v = RnsPoly.zeros(raised, params.n_ring, "eval")
+    for off, m_hat in sorted(diags.items()):
+        assert m_hat.moduli == raised
+        if off % params.slots == 0:
+            acc_u = acc_u.add(m_hat.mul(pmodup(params, ct.a)))
+            acc_v = acc_v.add(m_hat.mul(pmodup(params, ct.b)))
+            continue
+        r = -off
+        t = _galois(params, r)
+        u, v = _kskip_raw(params, dig, keys.rot[r], limbs, t)
+        b_hat = pmodup(params, ct.b.automorph(t))
+        acc_u = acc_u.add(m_hat.mul(RnsPoly(raised, u, "eval")))
+        acc_v = acc_v.add(m_hat.mul(RnsPoly(raised, v, "eval").add(b_hat)))
+    a_out = _moddown_merged(params, acc_u, limbs)
+    b_out = _moddown_merged(params, acc_v, limbs)
+    return Ciphertext(a_out, b_out, ct.delta * diag_delta / raised[limbs - 1])
+
+
+def bsgs(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict, diag_delta: float,
+         baby: int, giant: int) -> Ciphertext:
+    """Hoisted BSGS linear transform (composites.py:249-293).
+
+    One shared ModUp; baby KSKIPs (k = 1..baby) reused by every giant group;
+    per group j the raised accumulators sum diags[(j, k)] * (u_k, v_k + P b_k),
+    one merged ModDown, then a full rotate by -baby*j at l-1; results summed.
+    Bit-identical to sum_j rotate(pt_matvec(ct, {k: diags[j,k]}), -baby*j).
+    """
+    limbs = ct.limbs
+    raised = params.raised_moduli(limbs)
+    dig = _decomp_modup_raw(params, ct.a.data, limbs)
+    baby_uv = {}
+    for k in range(1, baby + 1):
+        t = _galois(params, -k)
+        u, v = _kskip_raw(params, dig, keys.rot[-k], limbs, t)
+        vb = RnsPoly(raised, v, "eval").add(pmodup(params, ct.b.automorph(t)))
+        baby_uv[k] = (RnsPoly(raised, u, "eval"), vb)
+    out = None
+    for j in range(1, giant + 1):
+        acc_u = RnsPoly.zeros(raised, params.n_ring, "eval")
+        acc_v = RnsPoly.zeros(raised, params.n_ring, "eval")
+        for k in range(1, baby + 1):
+            m_hat = diags[(j, k)]
+            acc_u = acc_u.add(m_hat.mul(baby_uv[k][0]))
+            acc_v = acc_v.add(m_hat.mul(baby_uv[k][1]))
+        g = Ciphertext(_moddown_merged(params, acc_u, limbs), _moddown_merged(params, acc_v, limbs),
+                       ct.delta * diag_delta / raised[limbs - 1])
+        rj = rotate(params, keys, g, -baby * j)
+        out = rj if out is None else add(out, rj)
+    return out
+
+
+def raise_modulus(params: CkksParams, ct: Ciphertext, limbs: int) -> Ciphertext:
+    """ckks.raise_modulus (ckks.py:722-740): centered basis extension."""
+    from .rnspoly import bc_convert_centered
+    assert ct.limbs < limbs
+    src = ct.a.moduli
+    extra = params.chain[ct.limbs:limbs]
+
+    def up(x: RnsPoly) -> RnsPoly:
+        coeff = RnsPoly(src, ntt_rows(x.data, src, True), "coeff")
+        conv = bc_convert_centered(coeff, extra)
+        conv_e = ntt_rows(conv.data, extra, False)
+        return RnsPoly(src + extra, torch.cat([x.data, conv_e]), "eval")
+
+    return Ciphertext(up(ct.a), up(ct.b), ct.delta)
+
+
+# ------------------------------------------------------- batched entry
+
+def rotate_batch(params: CkksParams, a: torch.Tensor, b: torch.Tensor, key_b: torch.Tensor,
+                 key_a: torch.Tensor, galois: torch.Tensor, out_a: torch.Tensor,
+                 out_b: torch.Tensor, ws: torch.Tensor | None = None) -> None:
+    """B independent rotation key-switches in one call (BASELINE config 3/5 unit).
+
+    a, b, out_a, out_b: (B, l, N); key_b, key_a: (B, dnum, L+K, N);
+    galois: (B,) uint64 Galois elements (5^k mod 2N).
+    """
+    plan = plan_for(params)
+    B, limbs = a.shape[0], a.shape[1]
+    ws = plan.workspace(limbs, B, "batch") if ws is None else ws
+    check(_L().ck_rotate(plan.h, ptr(a), ptr(b), ptr(key_b), ptr(key_a), limbs, 1, ptr(galois), 0,
+                         ptr(out_a), ptr(out_b), ptr(ws), B, stream_handle()), "ck_rotate")
+
+
+def automorph(x: RnsPoly, t: int) -> RnsPoly:
+    return RnsPoly(x.moduli, automorph_rows(x.data, t, x.moduli), x.rep)

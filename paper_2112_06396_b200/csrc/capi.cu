@@ -1,0 +1,763 @@
+// C ABI: plan creation (host tables) and the key-switching pipeline.
+//
+// Host-side table construction restates, with exact 128-bit integer
+// arithmetic, the reference's setup code:
+//   psi / twiddles ........ zq.primitive_root_2n (zq.py:79-84),
+//                           NttContext.__init__ (rnspoly.py:34-46)
+//   BC tables ............. _bc_tables (rnspoly.py:248-261),
+//                           _bc_center_tables (rnspoly.py:290-300)
+//   digit spans / rows .... CkksParams.digit_spans (ckks.py:56-62),
+//                           _key_rows (ckks.py:444-447)
+//   P^-1, [P]_q ........... _moddown_poly (ckks.py:411-416), pmodup (ckks.py:478-489)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "ck_internal.h"
+#include "ntt.cuh"
+
+typedef unsigned __int128 u128;
+
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+namespace ck {
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace ck
+
+namespace {
+
+// ------------------------------------------------------------ host number theory
+u64 mulmod_h(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+u64 powmod_h(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = mulmod_h(r, a, q);
+    a = mulmod_h(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+u64 invmod_h(u64 a, u64 q) { return powmod_h(a, q - 2, q); }
+u64 shoup_h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+
+bool isprime_h(u64 n) {
+  if (n < 2) return false;
+  static const u64 bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (u64 p : bases)
+    if (n % p == 0) return n == p;
+  u64 d = n - 1;
+  int r = 0;
+  while ((d & 1) == 0) { d >>= 1; ++r; }
+  for (u64 a : bases) {
+    u64 x = powmod_h(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < r; ++i) {
+      x = mulmod_h(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
+std::vector<u64> prime_factors(u64 m) {
+  std::vector<u64> f;
+  if (m % 2 == 0) { f.push_back(2); while (m % 2 == 0) m /= 2; }
+  for (u64 d = 3; d * d <= m; d += 2) {
+    if (m % d == 0) { f.push_back(d); while (m % d == 0) m /= d; }
+    if (m > 1 && isprime_h(m)) break;
+  }
+  if (m > 1) f.push_back(m);
+  return f;
+}
+
+// psi = g^((q-1)/2N), g the smallest primitive root (== sympy.primitive_root)
+u64 psi_for(u64 q, int logn) {
+  const std::vector<u64> f = prime_factors(q - 1);
+  for (u64 g = 2;; ++g) {
+    bool ok = true;
+    for (u64 p : f)
+      if (powmod_h(g, (q - 1) / p, q) == 1) { ok = false; break; }
+    if (ok) return powmod_h(g, (q - 1) >> (logn + 1), q);
+  }
+}
+
+u32 brev_h(u32 x, int bits) {
+  u32 r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- plan types
+struct ck_bconv {
+  int ns = 0, nd = 0, centered = 0;
+  int* d_src = nullptr;
+  int* d_dst = nullptr;
+  ulonglong2* d_ihat = nullptr;   // plain ihat (generic apply)
+  u64* d_T = nullptr;
+  double* d_w = nullptr;
+  u64* d_kQ = nullptr;
+  long long* d_out_off = nullptr; // optional
+  std::vector<void*> allocs;
+  ~ck_bconv() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+namespace {
+
+struct ModDownTab {
+  bool valid = false;
+  int keep = 0, ndrop = 0, drop_row0 = 0;
+  ck_bconv* bc = nullptr;             // centered, drop -> keep
+  ulonglong2* d_drop_scale = nullptr; // ihat * n^-1 per drop row
+  long long* d_drop_off = nullptr;    // row offsets of the drop rows
+  int* d_drop_prime = nullptr;
+  int* d_keep_prime = nullptr;
+  ulonglong2* d_pinv = nullptr;       // [P_drop]^-1 mod q_j per keep row
+};
+
+struct LevelTab {
+  int l = 0, beta = 0, R = 0;
+  std::vector<int> lo, hi;
+  int* d_chain_prime = nullptr;       // [l]
+  int* d_raised_prime = nullptr;      // [R] (== full-basis key row)
+  ulonglong2* d_modup_scale = nullptr;// [l] ihat(digit) * n^-1
+  std::vector<ck_bconv*> modup_bc;    // per digit, targets = raised \ own
+  long long* d_modup_ntt_off = nullptr;
+  int* d_modup_ntt_prime = nullptr;
+  int modup_ntt_jobs = 0;
+  ulonglong2* d_pmod = nullptr;       // [P]_q per chain row
+  ModDownTab md[3];
+};
+
+}  // namespace
+
+struct ck_plan {
+  int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
+  std::vector<u64> mod, psi;
+  PrimeConst* d_pc = nullptr;
+  ulonglong2* d_tw = nullptr;
+  ulonglong2* d_itw = nullptr;
+  std::vector<LevelTab> lv;  // index = level
+  std::vector<void*> allocs;
+  std::vector<ck_bconv*> bcs;
+  ~ck_plan() {
+    for (ck_bconv* b : bcs) delete b;
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+namespace {
+
+template <class T>
+T* upload(std::vector<void*>& allocs, const std::vector<T>& v, int* err) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  if (cudaMalloc(&p, v.size() * sizeof(T)) != cudaSuccess) { *err = CK_ERR_ALLOC; return nullptr; }
+  allocs.push_back(p);
+  cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return (T*)p;
+}
+
+PrimeConst make_pc(u64 q, int logn) {
+  PrimeConst P;
+  std::memset(&P, 0, sizeof(P));
+  P.q = q;
+  P.two_q = 2 * q;
+  P.bar = (u64)(((u128)1 << 64) / q);
+  P.c30 = ((u64)1 << 30) % q;
+  P.c30p = shoup_h(P.c30, q);
+  P.c60 = ((u64)1 << 60) % q;
+  P.c60p = shoup_h(P.c60, q);
+  P.r64 = (u64)(((u128)1 << 64) % q);
+  P.r64p = shoup_h(P.r64, q);
+  P.ninv = invmod_h(((u64)1 << logn) % q, q);
+  P.ninvp = shoup_h(P.ninv, q);
+  return P;
+}
+
+ulonglong2 sh2(u64 w, u64 q) { return make_ulonglong2(w, shoup_h(w, q)); }
+
+// BC tables between plan primes (rnspoly.py:248-261, 290-300)
+ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector<int>& dst,
+                      bool centered, int* err) {
+  ck_bconv* b = new ck_bconv();
+  b->ns = (int)src.size();
+  b->nd = (int)dst.size();
+  b->centered = centered;
+  std::vector<ulonglong2> ihat(src.size());
+  std::vector<u64> T(src.size() * dst.size());
+  std::vector<double> w(src.size());
+  for (size_t i = 0; i < src.size(); ++i) {
+    const u64 qi = p->mod[src[i]];
+    u64 prod = 1 % qi;  // (Q/q_i) mod q_i
+    for (size_t k = 0; k < src.size(); ++k)
+      if (k != i) prod = mulmod_h(prod, p->mod[src[k]] % qi, qi);
+    ihat[i] = sh2(invmod_h(prod, qi), qi);
+    for (size_t j = 0; j < dst.size(); ++j) {
+      const u64 pj = p->mod[dst[j]];
+      u64 t = 1 % pj;
+      for (size_t k = 0; k < src.size(); ++k)
+        if (k != i) t = mulmod_h(t, p->mod[src[k]] % pj, pj);
+      T[i * dst.size() + j] = t;
+    }
+    w[i] = 1.0 / (double)qi;  // Python: 1.0 / q  (q rounded to double first)
+  }
+  std::vector<u64> kQ(dst.size() * (src.size() + 1));
+  for (size_t j = 0; j < dst.size(); ++j) {
+    const u64 pj = p->mod[dst[j]];
+    u64 qm = 1 % pj;
+    for (size_t k = 0; k < src.size(); ++k) qm = mulmod_h(qm, p->mod[src[k]] % pj, pj);
+    for (size_t k = 0; k <= src.size(); ++k) kQ[j * (src.size() + 1) + k] = mulmod_h(k % pj, qm, pj);
+  }
+  b->d_src = upload(b->allocs, src, err);
+  b->d_dst = upload(b->allocs, dst, err);
+  b->d_ihat = upload(b->allocs, ihat, err);
+  b->d_T = upload(b->allocs, T, err);
+  b->d_w = upload(b->allocs, w, err);
+  b->d_kQ = upload(b->allocs, kQ, err);
+  return b;
+}
+
+void build_moddown(ck_plan* p, ModDownTab& t, const std::vector<int>& keep,
+                   const std::vector<int>& drop, int drop_row0, int* err) {
+  t.valid = true;
+  t.keep = (int)keep.size();
+  t.ndrop = (int)drop.size();
+  t.drop_row0 = drop_row0;
+  t.bc = build_bconv(p, drop, keep, true, err);
+  p->bcs.push_back(t.bc);
+  std::vector<ulonglong2> dscale(drop.size());
+  std::vector<long long> doff(drop.size());
+  for (size_t i = 0; i < drop.size(); ++i) {
+    const u64 qi = p->mod[drop[i]];
+    u64 prod = 1 % qi;
+    for (size_t k = 0; k < drop.size(); ++k)
+      if (k != i) prod = mulmod_h(prod, p->mod[drop[k]] % qi, qi);
+    const u64 ninv = invmod_h((u64)p->n % qi, qi);
+    dscale[i] = sh2(mulmod_h(invmod_h(prod, qi), ninv, qi), qi);
+    doff[i] = (long long)(drop_row0 + (int)i) << p->logn;
+  }
+  std::vector<ulonglong2> pinv(keep.size());
+  for (size_t j = 0; j < keep.size(); ++j) {
+    const u64 qj = p->mod[keep[j]];
+    u64 bp = 1 % qj;
+    for (int d : drop) bp = mulmod_h(bp, p->mod[d] % qj, qj);
+    pinv[j] = sh2(invmod_h(bp, qj), qj);
+  }
+  t.d_drop_scale = upload(p->allocs, dscale, err);
+  t.d_drop_off = upload(p->allocs, doff, err);
+  t.d_drop_prime = upload(p->allocs, drop, err);
+  t.d_keep_prime = upload(p->allocs, keep, err);
+  t.d_pinv = upload(p->allocs, pinv, err);
+}
+
+int build_level(ck_plan* p, int l) {
+  int err = 0;
+  LevelTab& t = p->lv[l];
+  t.l = l;
+  t.R = l + p->K;
+  for (int j = 0; j < l; j += p->alpha) {
+    t.lo.push_back(j);
+    t.hi.push_back(std::min(j + p->alpha, l));
+  }
+  t.beta = (int)t.lo.size();
+  std::vector<int> chain(l), raised;
+  for (int i = 0; i < l; ++i) chain[i] = i;
+  raised = chain;
+  for (int k = 0; k < p->K; ++k) raised.push_back(p->L + k);
+  t.d_chain_prime = upload(p->allocs, chain, &err);
+  t.d_raised_prime = upload(p->allocs, raised, &err);
+  // ModUp: per digit, own = chain[lo:hi], targets = raised minus own (raised order)
+  std::vector<ulonglong2> mscale(l);
+  std::vector<long long> ntt_off;
+  std::vector<int> ntt_prime;
+  for (int d = 0; d < t.beta; ++d) {
+    std::vector<int> own, tgt;
+    std::vector<long long> out_off;
+    for (int i = t.lo[d]; i < t.hi[d]; ++i) own.push_back(i);
+    for (int r = 0; r < t.R; ++r) {
+      if (r >= t.lo[d] && r < t.hi[d]) continue;
+      tgt.push_back(raised[r]);
+      out_off.push_back((long long)r << p->logn);
+      ntt_off.push_back(((long long)d * t.R + r) << p->logn);
+      ntt_prime.push_back(raised[r]);
+    }
+    ck_bconv* bc = build_bconv(p, own, tgt, false, &err);
+    bc->d_out_off = upload(bc->allocs, out_off, &err);
+    p->bcs.push_back(bc);
+    t.modup_bc.push_back(bc);
+    for (size_t i = 0; i < own.size(); ++i) {
+      const u64 qi = p->mod[own[i]];
+      u64 prod = 1 % qi;
+      for (size_t k = 0; k < own.size(); ++k)
+        if (k != i) prod = mulmod_h(prod, p->mod[own[k]] % qi, qi);
+      const u64 ninv = invmod_h((u64)p->n % qi, qi);
+      mscale[own[i]] = sh2(mulmod_h(invmod_h(prod, qi), ninv, qi), qi);
+    }
+  }
+  t.d_modup_scale = upload(p->allocs, mscale, &err);
+  t.d_modup_ntt_off = upload(p->allocs, ntt_off, &err);
+  t.d_modup_ntt_prime = upload(p->allocs, ntt_prime, &err);
+  t.modup_ntt_jobs = (int)ntt_off.size();
+  // [P]_q per chain row (pmodup)
+  std::vector<ulonglong2> pm(l);
+  for (int i = 0; i < l; ++i) {
+    u64 bp = 1 % p->mod[i];
+    for (int k = 0; k < p->K; ++k) bp = mulmod_h(bp, p->mod[p->L + k] % p->mod[i], p->mod[i]);
+    pm[i] = sh2(bp, p->mod[i]);
+  }
+  t.d_pmod = upload(p->allocs, pm, &err);
+  // ModDown variants
+  std::vector<int> spec;
+  for (int k = 0; k < p->K; ++k) spec.push_back(p->L + k);
+  if (p->K > 0) build_moddown(p, t.md[0], chain, spec, l, &err);
+  if (l >= 2) {
+    std::vector<int> keep(chain.begin(), chain.end() - 1), drop{l - 1};
+    drop.insert(drop.end(), spec.begin(), spec.end());
+    build_moddown(p, t.md[1], keep, drop, l - 1, &err);
+    build_moddown(p, t.md[2], keep, std::vector<int>{l - 1}, l - 1, &err);
+  }
+  return err;
+}
+
+// ------------------------------------------------------------------ launchers
+int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off,
+             const ulonglong2* scale, int jobs, int batch, long long bstride, bool inv,
+             cudaStream_t st) {
+  ck::NttArgs a;
+  a.data = base;
+  a.prime_idx = prime;
+  a.row_off = off;
+  a.pc = p->d_pc;
+  a.tw = p->d_tw;
+  a.itw = p->d_itw;
+  a.scale = scale;
+  a.batch_stride = bstride;
+  a.logn = p->logn;
+  return ck::launch_ntt(a, jobs, batch, inv, st);
+}
+
+int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
+              u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st) {
+  ck::BconvArgs a;
+  a.in = in;
+  a.in_batch = in_batch;
+  a.in_off = nullptr;
+  a.out = out;
+  a.out_batch = out_batch;
+  a.out_off = bc->d_out_off;
+  a.src_prime = bc->d_src;
+  a.dst_prime = bc->d_dst;
+  a.pc = p->d_pc;
+  a.src_scale = prescale ? bc->d_ihat : nullptr;
+  a.T = bc->d_T;
+  a.w = bc->d_w;
+  a.kQ = bc->d_kQ;
+  a.ns = bc->ns;
+  a.nd = bc->nd;
+  a.logn = p->logn;
+  a.centered = bc->centered;
+  return ck::launch_bconv(a, batch, st);
+}
+
+int ew_run(const ck_plan* p, int op, u64* out, long long ob, const u64* x, long long xb,
+           const u64* y, long long yb, const u64* z, long long zb, const int* prime,
+           const ulonglong2* cst, u64 gt, const u64* galois, int rows, int batch,
+           cudaStream_t st) {
+  ck::EwArgs a;
+  a.out = out;
+  a.x = x;
+  a.y = y;
+  a.z = z;
+  a.out_batch = ob;
+  a.x_batch = xb;
+  a.y_batch = yb;
+  a.z_batch = zb;
+  a.prime = prime;
+  a.pc = p->d_pc;
+  a.cst = cst;
+  a.galois_t = gt;
+  a.galois = galois;
+  a.op = op;
+  a.logn = p->logn;
+  return ck::launch_ew(a, rows, batch, st);
+}
+
+#define CK_TRY(x)            \
+  do {                       \
+    int _e = (x);            \
+    if (_e) return _e;       \
+  } while (0)
+
+bool level_ok(const ck_plan* p, int l) { return p && l >= 1 && l <= p->L; }
+
+// workspace regions (elements), each [batch][rows][N]
+struct Ws {
+  u64 *tmp, *conv, *rot, *uv, *dig;
+};
+Ws ws_layout(const ck_plan* p, int l, int batch, u64* base) {
+  const LevelTab& t = p->lv[l];
+  const long long N = p->n, B = batch;
+  Ws w;
+  w.tmp = base;
+  w.conv = w.tmp + B * l * N;
+  w.rot = w.conv + B * 2 * l * N;
+  w.uv = w.rot + B * 2 * l * N;
+  w.dig = w.uv + B * 2 * t.R * N;
+  return w;
+}
+
+// ModUp: digits [B][beta][R][N] from a [B][l][N] (eval).  tmp: [B][l][N].
+int modup_impl(const ck_plan* p, int l, const u64* a, u64* digits, u64* tmp, int B,
+               cudaStream_t st) {
+  const LevelTab& t = p->lv[l];
+  const long long N = p->n;
+  const long long dig_b = (long long)t.beta * t.R * N;
+  CK_TRY((int)cudaMemcpyAsync(tmp, a, sizeof(u64) * B * l * N, cudaMemcpyDeviceToDevice, st));
+  // INTT of every chain row, scaled by its digit's ihat (rnspoly.py:274-275)
+  CK_TRY(ntt_rows(p, tmp, t.d_chain_prime, nullptr, t.d_modup_scale, l, B, l * N, true, st));
+  for (int d = 0; d < t.beta; ++d)
+    CK_TRY(bconv_run(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
+                     false, B, st));
+  CK_TRY(ntt_rows(p, digits, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
+                  dig_b, false, st));
+  for (int d = 0; d < t.beta; ++d) {
+    const int own = t.hi[d] - t.lo[d];
+    CK_TRY((int)cudaMemcpy2DAsync(digits + d * t.R * N + t.lo[d] * N, dig_b * sizeof(u64),
+                                  a + t.lo[d] * N, l * N * sizeof(u64), own * N * sizeof(u64), B,
+                                  cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+int kskip_impl(const ck_plan* p, int l, const u64* digits, const u64* kb, const u64* ka,
+               u64 gt, const u64* galois, u64* u, u64* v, long long uv_batch, int B,
+               cudaStream_t st) {
+  const LevelTab& t = p->lv[l];
+  const long long N = p->n;
+  ck::KskipArgs a;
+  a.digits = digits;
+  a.digit_stride = (long long)t.R * N;
+  a.digits_batch = (long long)t.beta * t.R * N;
+  a.key_b = kb;
+  a.key_a = ka;
+  a.key_digit_stride = (long long)(p->L + p->K) * N;
+  a.key_batch = (long long)p->key_digits * (p->L + p->K) * N;
+  a.key_row = t.d_raised_prime;
+  a.prime = t.d_raised_prime;
+  a.pc = p->d_pc;
+  a.u = u;
+  a.v = v;
+  a.out_batch = uv_batch;
+  a.galois = galois;
+  a.galois_t = gt % (2ull * p->n);
+  a.beta = t.beta;
+  a.logn = p->logn;
+  return ck::launch_kskip(a, t.R, B, st);
+}
+
+// ModDown steps 1-3 on a flattened batch: x [B][xrows][N] -> conv [B][keep][N]
+int moddown_core(const ck_plan* p, const ModDownTab& m, u64* x, long long xb, u64* conv, int B,
+                 cudaStream_t st) {
+  const long long N = p->n;
+  CK_TRY(ntt_rows(p, x, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, B, xb, true, st));
+  CK_TRY(bconv_run(p, m.bc, x + (long long)m.drop_row0 * N, xb, conv, (long long)m.keep * N, false,
+                   B, st));
+  return ntt_rows(p, conv, m.d_keep_prime, nullptr, nullptr, m.keep, B, (long long)m.keep * N,
+                  false, st);
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+int ck_version(void) { return 1; }
+
+int64_t ck_launch_count(void) { return g_launches.load(); }
+
+const char* ck_error_string(int code) {
+  switch (code) {
+    case CK_OK: return "ok";
+    case CK_ERR_ARG: return "invalid argument";
+    case CK_ERR_MODULUS: return "invalid modulus";
+    case CK_ERR_ALLOC: return "device allocation failed";
+    case CK_ERR_DEVICE: return "no CUDA device";
+    default: return code > 0 ? cudaGetErrorString((cudaError_t)code) : "unknown error";
+  }
+}
+
+int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
+                   int n_special, int dnum, ck_plan** out) {
+  if (!out || log_n < 1 || log_n > 17 || n_chain < 1 || n_special < 0 || dnum < 1 || !chain ||
+      (n_special > 0 && !special))
+    return CK_ERR_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return CK_ERR_DEVICE;
+  ck_plan* p = new ck_plan();
+  p->logn = log_n;
+  p->n = 1 << log_n;
+  p->L = n_chain;
+  p->K = n_special;
+  p->dnum = dnum;
+  p->alpha = (n_chain + dnum - 1) / dnum;
+  p->key_digits = (n_chain + p->alpha - 1) / p->alpha;
+  for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
+  for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
+  const u64 two_n = 2ull << log_n;
+  for (size_t i = 0; i < p->mod.size(); ++i) {
+    const u64 q = p->mod[i];
+    if (q >= (1ull << 60) || q % two_n != 1 || !isprime_h(q)) { delete p; return CK_ERR_MODULUS; }
+    for (size_t j = 0; j < i; ++j)
+      if (p->mod[j] == q) { delete p; return CK_ERR_MODULUS; }
+  }
+  const int np = (int)p->mod.size();
+  const long long N = p->n;
+  p->psi.resize(np);
+  std::vector<PrimeConst> pcs(np);
+  std::vector<ulonglong2> tw((size_t)np * N), itw((size_t)np * N);
+  std::vector<u32> br(N);
+  for (u32 i = 0; i < (u32)N; ++i) br[i] = brev_h(i, log_n);
+  auto work = [&](int i) {
+    const u64 q = p->mod[i];
+    const u64 psi = psi_for(q, log_n);
+    p->psi[i] = psi;
+    pcs[i] = make_pc(q, log_n);
+    std::vector<u64> pw(N), ipw(N);
+    const u64 ipsi = invmod_h(psi, q);
+    pw[0] = ipw[0] = 1;
+    for (long long k = 1; k < N; ++k) {
+      pw[k] = mulmod_h(pw[k - 1], psi, q);
+      ipw[k] = mulmod_h(ipw[k - 1], ipsi, q);
+    }
+    for (long long k = 0; k < N; ++k) {
+      tw[(size_t)i * N + k] = sh2(pw[br[k]], q);
+      itw[(size_t)i * N + k] = sh2(ipw[br[k]], q);
+    }
+  };
+  {
+    const int nth = std::max(1, std::min(np, (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back([&, t] {
+        for (int i = t; i < np; i += nth) work(i);
+      });
+    for (auto& x : th) x.join();
+  }
+  int err = 0;
+  p->d_pc = upload(p->allocs, pcs, &err);
+  p->d_tw = upload(p->allocs, tw, &err);
+  p->d_itw = upload(p->allocs, itw, &err);
+  p->lv.resize(n_chain + 1);
+  for (int l = 1; l <= n_chain && !err; ++l) err = build_level(p, l);
+  if (err) { delete p; return err; }
+  *out = p;
+  return 0;
+}
+
+int ck_plan_destroy(ck_plan* plan) {
+  delete plan;
+  return 0;
+}
+
+int ck_plan_info(const ck_plan* p, int64_t* out) {
+  if (!p || !out) return CK_ERR_ARG;
+  out[0] = p->n;
+  out[1] = p->L;
+  out[2] = p->K;
+  out[3] = p->dnum;
+  out[4] = p->alpha;
+  return 0;
+}
+
+int ck_plan_psi(const ck_plan* p, uint64_t* psi_out) {
+  if (!p || !psi_out) return CK_ERR_ARG;
+  for (size_t i = 0; i < p->psi.size(); ++i) psi_out[i] = p->psi[i];
+  return 0;
+}
+
+int ck_plan_twiddles(const ck_plan* p, int prime, int inverse, uint64_t* out) {
+  if (!p || !out || prime < 0 || prime >= (int)p->mod.size()) return CK_ERR_ARG;
+  std::vector<ulonglong2> h(p->n);
+  const ulonglong2* src = (inverse ? p->d_itw : p->d_tw) + (size_t)prime * p->n;
+  CK_TRY((int)cudaMemcpy(h.data(), src, sizeof(ulonglong2) * p->n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < p->n; ++i) out[i] = h[i].x;
+  return 0;
+}
+
+int ck_ntt(const ck_plan* p, uint64_t* data_, const int32_t* prime_idx, int rows, int batch,
+           int64_t batch_stride, int inverse, ck_stream stream) {
+  u64* data = (u64*)data_;
+  if (!p || !data || !prime_idx || rows < 0 || batch < 0) return CK_ERR_ARG;
+  return ntt_rows(p, data, prime_idx, nullptr, nullptr, rows, batch, batch_stride, inverse != 0,
+                  (cudaStream_t)stream);
+}
+
+int ck_poly_op(const ck_plan* p, int op, uint64_t* out_, const uint64_t* x_, const uint64_t* y_,
+               const int32_t* prime_idx, const uint64_t* cst, int rows, ck_stream stream) {
+  u64* out = (u64*)out_;
+  const u64* x = (const u64*)x_;
+  const u64* y = (const u64*)y_;
+  if (!p || !out || !x || !prime_idx || op < 0 || op > 5) return CK_ERR_ARG;
+  if ((op <= 2) && !y) return CK_ERR_ARG;
+  if (op == 4 && !cst) return CK_ERR_ARG;
+  return ew_run(p, op, out, 0, x, 0, y, 0, nullptr, 0, prime_idx, (const ulonglong2*)cst, 1,
+                nullptr, rows, 1, (cudaStream_t)stream);
+}
+
+int ck_automorph(const ck_plan* p, uint64_t* out_, const uint64_t* x_, int rows, uint64_t galois_t,
+                 ck_stream stream) {
+  u64* out = (u64*)out_;
+  const u64* x = (const u64*)x_;
+  if (!p || !out || !x || rows < 0 || (galois_t & 1) == 0) return CK_ERR_ARG;
+  if (rows == 0) return 0;
+  return ew_run(p, ck::EW_AUTOMORPH, out, 0, x, 0, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                galois_t % (2ull * p->n), nullptr, 1, rows, (cudaStream_t)stream);
+}
+
+int ck_bconv_create(const ck_plan* p, const int32_t* src_idx, int ns, const int32_t* dst_idx,
+                    int nd, int centered, ck_bconv** out) {
+  if (!p || !src_idx || !dst_idx || ns < 1 || nd < 1 || !out) return CK_ERR_ARG;
+  std::vector<int> s(src_idx, src_idx + ns), d(dst_idx, dst_idx + nd);
+  for (int v : s)
+    if (v < 0 || v >= (int)p->mod.size()) return CK_ERR_ARG;
+  for (int v : d)
+    if (v < 0 || v >= (int)p->mod.size()) return CK_ERR_ARG;
+  int err = 0;
+  ck_bconv* b = build_bconv(const_cast<ck_plan*>(p), s, d, centered != 0, &err);
+  if (err) { delete b; return err; }
+  *out = b;
+  return 0;
+}
+
+int ck_bconv_destroy(ck_bconv* bc) {
+  delete bc;
+  return 0;
+}
+
+int ck_bconv_apply(const ck_plan* p, const ck_bconv* bc, const uint64_t* in_, uint64_t* out_,
+                   ck_stream stream) {
+  const u64* in = (const u64*)in_;
+  u64* out = (u64*)out_;
+  if (!p || !bc || !in || !out) return CK_ERR_ARG;
+  return bconv_run(p, bc, in, 0, out, 0, true, 1, (cudaStream_t)stream);
+}
+
+size_t ck_workspace_bytes(const ck_plan* p, int level, int batch) {
+  if (!level_ok(p, level) || batch < 1) return 0;
+  const LevelTab& t = p->lv[level];
+  const long long rows = level + 2LL * level + 2LL * level + 2LL * t.R + (long long)t.beta * t.R;
+  return (size_t)rows * p->n * sizeof(u64) * batch;
+}
+
+int ck_modup(const ck_plan* p, const uint64_t* a_eval_, int level, uint64_t* digits_,
+             uint64_t* workspace_, int batch, ck_stream stream) {
+  const u64* a_eval = (const u64*)a_eval_;
+  u64* digits = (u64*)digits_;
+  u64* workspace = (u64*)workspace_;
+  if (!level_ok(p, level) || !a_eval || !digits || !workspace || batch < 1) return CK_ERR_ARG;
+  const Ws w = ws_layout(p, level, batch, workspace);
+  return modup_impl(p, level, a_eval, digits, w.tmp, batch, (cudaStream_t)stream);
+}
+
+int ck_kskip(const ck_plan* p, const uint64_t* digits_, const uint64_t* key_b_,
+             const uint64_t* key_a_, int level, uint64_t galois_t, const uint64_t* galois_,
+             uint64_t* u_, uint64_t* v_, int batch, ck_stream stream) {
+  const u64 *digits = (const u64*)digits_, *key_b = (const u64*)key_b_, *key_a = (const u64*)key_a_,
+            *galois = (const u64*)galois_;
+  u64 *u = (u64*)u_, *v = (u64*)v_;
+  if (!level_ok(p, level) || !digits || !key_b || !key_a || !u || !v || batch < 1 ||
+      (galois_t & 1) == 0)
+    return CK_ERR_ARG;
+  const long long ub = (long long)p->lv[level].R * p->n;
+  return kskip_impl(p, level, digits, key_b, key_a, galois_t, galois, u, v, ub, batch,
+                    (cudaStream_t)stream);
+}
+
+int ck_moddown(const ck_plan* p, uint64_t* x_, int level, int merged, uint64_t* out_,
+               const uint64_t* addend_, uint64_t galois_t, uint64_t* workspace_, int batch,
+               ck_stream stream) {
+  u64 *x = (u64*)x_, *out = (u64*)out_, *workspace = (u64*)workspace_;
+  const u64* addend = (const u64*)addend_;
+  if (!level_ok(p, level) || !x || !out || !workspace || merged < 0 || merged > 2 || batch < 1 ||
+      (galois_t & 1) == 0)
+    return CK_ERR_ARG;
+  const LevelTab& t = p->lv[level];
+  const ModDownTab& m = t.md[merged];
+  if (!m.valid) return CK_ERR_ARG;
+  const long long N = p->n;
+  const long long xrows = merged == 2 ? level : t.R;
+  const Ws w = ws_layout(p, level, batch, workspace);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK_TRY(moddown_core(p, m, x, xrows * N, w.conv, batch, st));
+  return ew_run(p, ck::EW_MODDOWN, out, m.keep * N, x, xrows * N, w.conv, m.keep * N, addend,
+                m.keep * N, m.d_keep_prime, m.d_pinv, galois_t % (2ull * p->n), nullptr, m.keep,
+                batch, st);
+}
+
+int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
+              const uint64_t* key_a_, int level, uint64_t galois_t, const uint64_t* galois_,
+              int mode, uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, int batch,
+              ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *key_b = (const u64*)key_b_,
+            *key_a = (const u64*)key_a_, *galois = (const u64*)galois_;
+  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *workspace = (u64*)workspace_;
+  if (!level_ok(p, level) || !a || !b || !key_b || !key_a || !out_a || !out_b || !workspace ||
+      batch < 1 || (mode != 0 && mode != 1) || (galois_t & 1) == 0 || p->K < 1)
+    return CK_ERR_ARG;
+  if (mode == 1 && galois) return CK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const LevelTab& t = p->lv[level];
+  const long long N = p->n, l = level, R = t.R;
+  const Ws w = ws_layout(p, level, batch, workspace);
+  const u64 gt = galois_t % (2ull * p->n);
+  const u64* a_src = a;
+  const u64* b_add = b;
+  u64 kgt = gt, egt = gt;
+  const u64* kgal = galois;
+  if (mode == 1) {
+    // conjugate: automorph first (ckks.py:677-678)
+    CK_TRY(ew_run(p, ck::EW_AUTOMORPH, w.rot, l * N, a, l * N, nullptr, 0, nullptr, 0,
+                  t.d_chain_prime, nullptr, gt, nullptr, level, batch, st));
+    CK_TRY(ew_run(p, ck::EW_AUTOMORPH, w.rot + batch * l * N, l * N, b, l * N, nullptr, 0,
+                  nullptr, 0, t.d_chain_prime, nullptr, gt, nullptr, level, batch, st));
+    a_src = w.rot;
+    b_add = w.rot + batch * l * N;
+    kgt = 1;
+    egt = 1;
+    kgal = nullptr;
+  }
+  CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
+  // uv: [B][2][R][N]
+  CK_TRY(kskip_impl(p, level, w.dig, key_b, key_a, kgt, kgal, w.uv, w.uv + R * N, 2 * R * N,
+                    batch, st));
+  const ModDownTab& m = t.md[0];
+  CK_TRY(moddown_core(p, m, w.uv, R * N, w.conv, 2 * batch, st));
+  // conv: [B][2][l][N]
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, l * N, w.uv, 2 * R * N, w.conv, 2 * l * N, nullptr, 0,
+                m.d_keep_prime, m.d_pinv, 1, nullptr, level, batch, st));
+  return ew_run(p, ck::EW_MODDOWN, out_b, l * N, w.uv + R * N, 2 * R * N, w.conv + l * N,
+                2 * l * N, b_add, l * N, m.d_keep_prime, m.d_pinv, egt, mode == 1 ? nullptr : galois,
+                level, batch, st);
+}
+
+int ck_fill_uniform(uint64_t* out_, int64_t rows, int log_n, const uint64_t* keys_,
+                    const uint64_t* qs_, ck_stream stream) {
+  u64* out = (u64*)out_;
+  const u64 *keys = (const u64*)keys_, *qs = (const u64*)qs_;
+  if (!out || !keys || !qs || rows < 0 || log_n < 1 || log_n > 20) return CK_ERR_ARG;
+  return ck::launch_fill_uniform(out, rows, log_n, keys, qs, (cudaStream_t)stream);
+}
+
+}  // extern "C"

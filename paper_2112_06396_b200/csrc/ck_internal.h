@@ -1,0 +1,86 @@
+// Internal declarations shared by the CUDA translation units and plan.cpp.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "../../include/ckks_b200.h"
+
+#ifdef __CUDACC__
+#include "modarith.cuh"
+#else
+typedef unsigned long long u64;
+struct PrimeConst {
+  u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, pad;
+};
+#endif
+
+namespace ck {
+
+// process-wide count of kernel launches (ck_launch_count)
+void count_launches(int n);
+
+struct NttArgs;
+int launch_ntt(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st);
+
+// Basis conversion: ns source rows (coefficient rep, same coefficient index)
+// -> nd destination rows.  T[i*nd+j] = (Q/q_i) mod p_j.
+struct BconvArgs {
+  const u64* in;
+  long long in_batch;           // elements between batch items
+  const long long* in_off;      // [ns] element offsets (nullable: i*N)
+  u64* out;
+  long long out_batch;
+  const long long* out_off;     // [nd] element offsets (nullable: j*N)
+  const int* src_prime;         // [ns]
+  const int* dst_prime;         // [nd]
+  const PrimeConst* pc;
+  const ulonglong2* src_scale;  // [ns] ihat Shoup pairs; nullable = already scaled
+  const u64* T;                 // [ns*nd]
+  const double* w;              // [ns] 1.0/q_i   (centered only)
+  const u64* kQ;                // [nd*(ns+1)] k*Q mod p_j  (centered only)
+  int ns, nd, logn, centered;
+};
+int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st);
+
+// Key-switching inner product with a fused eval-domain automorphism.
+struct KskipArgs {
+  const u64* digits;            // [beta][R][N] raised-basis eval rows
+  long long digit_stride;       // elements between digits
+  long long digits_batch;
+  const u64* key_b;             // [dnum][LK][N] full-basis rows
+  const u64* key_a;
+  long long key_digit_stride;   // elements between key digits (LK*N)
+  long long key_batch;
+  const int* key_row;           // [R] full-basis row of raised row i
+  const int* prime;             // [R] prime index of raised row i
+  const PrimeConst* pc;
+  u64* u;                       // [R][N]
+  u64* v;
+  long long out_batch;
+  const u64* galois;            // per batch item Galois element (nullable: galois_t)
+  u64 galois_t;                 // 1 = no automorphism
+  int beta, logn;
+};
+int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st);
+
+// Elementwise ops over limb rows.
+enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_MULC = 4, EW_COPY = 5,
+            EW_MODDOWN = 6, EW_AUTOMORPH = 7 };
+struct EwArgs {
+  u64* out;
+  const u64* x;
+  const u64* y;
+  const u64* z;                 // optional addend (moddown: gathered with galois)
+  long long out_batch, x_batch, y_batch, z_batch;
+  const int* prime;             // [rows]
+  const PrimeConst* pc;
+  const ulonglong2* cst;        // [rows] Shoup constants (MULC, MODDOWN)
+  u64 galois_t;                 // AUTOMORPH / MODDOWN addend gather (1 = none)
+  const u64* galois;            // per batch item (nullable: galois_t)
+  int op, logn;
+};
+int launch_ew(const EwArgs& a, int rows, int batch, cudaStream_t st);
+
+int launch_fill_uniform(u64* out, long long rows, int logn, const u64* keys, const u64* qs,
+                        cudaStream_t st);
+
+}  // namespace ck

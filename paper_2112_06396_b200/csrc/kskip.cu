@@ -1,0 +1,101 @@
+// Key-switching inner product (KSKIP) with the Galois automorphism folded in.
+//
+// Reference: ckks._kskip (ckks.py:450-465) on digits that hrotate first
+// permutes with RnsPoly.automorph (rnspoly.py:228-233):
+//   u[i][k] = sum_j d_j[i][perm(k)] * a_j[row_i][k]  mod q_i
+//   v[i][k] = sum_j d_j[i][perm(k)] * b_j[row_i][k]  mod q_i
+//
+// Storage-row structure of the eval-domain automorphism: with the storage
+// index split as i = r * 2^P2 + c (the NTT's row phase), perm maps a whole
+// output row r to a single input row r' (the affine map j -> t j + (t-1)/2
+// on natural indices keeps the low P1 bits of j, i.e. the storage row,
+// independent of c).  So each CTA stages the needed input rows in shared
+// memory with coalesced loads and gathers from there.
+#include "ck_internal.h"
+
+namespace ck {
+
+// any storage split works (see above); rows of <= 512 elements fit the tile
+CK_HD int ks_row_bits(int logn) { return logn < 9 ? logn : 9; }
+
+constexpr int kKsThreads = 256;
+constexpr int kKsMaxBeta = 8;
+
+// grid = (N / TILE, rows, batch); TILE = 512 elements (or N if smaller)
+template <int TILE>
+__global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
+  __shared__ u64 sd[kKsMaxBeta][TILE];
+  const int logn = a.logn;
+  const int p2 = ks_row_bits(logn);
+  const int rowlen = 1 << p2;
+  const int i = blockIdx.y;
+  const long long bz = blockIdx.z;
+  const int prime = a.prime[i];
+  const PrimeConst P = a.pc[prime];
+  const u64 t = a.galois ? a.galois[bz] : a.galois_t;
+  const long long tile0 = (long long)blockIdx.x * TILE;
+  const u64* dig = a.digits + bz * a.digits_batch + ((long long)i << logn);
+  // stage the gathered digit rows: for each storage row in the tile load the
+  // source row perm maps it to
+  for (int d = 0; d < a.beta; ++d) {
+    const u64* dd = dig + d * a.digit_stride;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      const long long o = tile0 + e;
+      const long long rowstart = o & ~(long long)(rowlen - 1);
+      const long long src_row = t == 1 ? rowstart
+                                       : (long long)(automorph_src((u32)rowstart, (u32)t, logn) &
+                                                     ~(u32)(rowlen - 1));
+      sd[d][e] = dd[src_row + (o & (rowlen - 1))];
+    }
+  }
+  __syncthreads();
+  const int krow = a.key_row[i];
+  const u64* kb = a.key_b + bz * a.key_batch + ((long long)krow << logn);
+  const u64* ka = a.key_a + bz * a.key_batch + ((long long)krow << logn);
+  u64* uo = a.u + bz * a.out_batch + ((long long)i << logn);
+  u64* vo = a.v + bz * a.out_batch + ((long long)i << logn);
+  for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+    const long long o = tile0 + e;
+    int se = e;
+    if (t != 1) {
+      const u32 src = automorph_src((u32)o, (u32)t, logn);
+      se = (int)((o & ~(long long)(rowlen - 1)) - tile0) + (int)(src & (rowlen - 1));
+    }
+    Acc3 su, sv;
+    acc3_zero(su);
+    acc3_zero(sv);
+    for (int d = 0; d < a.beta; ++d) {
+      const u64 x = sd[d][se];
+      const u64 ya = __ldg(ka + d * a.key_digit_stride + o);
+      const u64 yb = __ldg(kb + d * a.key_digit_stride + o);
+      const u32 x0 = lo30(x), x1 = hi30(x);
+      acc3_mac(su, x0, x1, lo30(ya), hi30(ya));
+      acc3_mac(sv, x0, x1, lo30(yb), hi30(yb));
+    }
+    uo[o] = acc3_reduce(su, P);
+    vo[o] = acc3_reduce(sv, P);
+  }
+}
+
+int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st) {
+  if (rows <= 0 || batch <= 0) return 0;
+  if (a.beta < 1 || a.beta > kKsMaxBeta) return CK_ERR_ARG;
+  const int n = 1 << a.logn;
+  count_launches(1);
+  if (n >= 512) {
+    kskip_kernel<512><<<dim3(n / 512, rows, batch), kKsThreads, 0, st>>>(a);
+  } else {
+    // small rings: one tile holds the whole limb (row_bits == logn)
+    switch (a.logn) {
+#define CK_KS_SMALL(L) \
+  case L: kskip_kernel<(1 << L)><<<dim3(1, rows, batch), kKsThreads, 0, st>>>(a); break;
+      CK_KS_SMALL(1) CK_KS_SMALL(2) CK_KS_SMALL(3) CK_KS_SMALL(4) CK_KS_SMALL(5)
+      CK_KS_SMALL(6) CK_KS_SMALL(7) CK_KS_SMALL(8)
+#undef CK_KS_SMALL
+      default: return CK_ERR_ARG;
+    }
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace ck

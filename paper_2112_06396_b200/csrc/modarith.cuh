@@ -1,0 +1,110 @@
+// 64-bit modular arithmetic on CUDA cores for word-sized NTT primes (q < 2^60).
+//
+// Replaces the reference's numpy vector ops (zq.py:145-194).  Every routine
+// returns the exact residue (canonical once fully reduced), so results are
+// bit-identical to the reference's float80-estimate mulmod (zq.py:161-177)
+// regardless of the reduction method used here.
+//
+// Lazy ("Harvey") ranges are used inside NTT butterflies: values live in
+// [0, 2q) or [0, 4q) between stages; 4q < 2^62 for q < 2^60.
+#pragma once
+#include <cstdint>
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+#define CK_HD __host__ __device__ __forceinline__
+#define CK_D __device__ __forceinline__
+
+// Per-prime constants, built on the host (plan.cpp) and read from global memory.
+struct PrimeConst {
+  u64 q;
+  u64 two_q;
+  u64 bar;        // floor(2^64 / q)           (Shoup companion of 1)
+  u64 c30, c30p;  // 2^30 mod q, Shoup companion
+  u64 c60, c60p;  // 2^60 mod q, Shoup companion
+  u64 r64, r64p;  // 2^64 mod q, Shoup companion
+  u64 ninv, ninvp;
+  u64 pad;
+};
+
+CK_D u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
+
+// x * w mod q in [0, 2q) for ANY 64-bit x; w < q, wp = floor(w * 2^64 / q).
+CK_D u64 shoup_lazy(u64 x, u64 w, u64 wp, u64 q) {
+  u64 qh = mulhi64(x, wp);
+  return x * w - qh * q;
+}
+
+CK_D u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+CK_D u64 shoup(u64 x, u64 w, u64 wp, u64 q) { return csub(shoup_lazy(x, w, wp, q), q); }
+
+CK_D u64 addmod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
+CK_D u64 submod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+
+// Any 64-bit x reduced into [0, 2q).
+CK_D u64 red64_lazy(u64 x, const PrimeConst& P) { return x - mulhi64(x, P.bar) * P.q; }
+CK_D u64 red64(u64 x, const PrimeConst& P) { return csub(red64_lazy(x, P), P.q); }
+
+// Full 128-bit value (hi:lo) mod q.
+CK_D u64 red128(u64 hi, u64 lo, const PrimeConst& P) {
+  u64 r = shoup_lazy(hi, P.r64, P.r64p, P.q) + red64_lazy(lo, P);  // < 4q
+  r = csub(r, P.two_q);
+  return csub(r, P.q);
+}
+
+CK_D u64 mulmod(u64 a, u64 b, const PrimeConst& P) {
+  return red128(mulhi64(a, b), a * b, P);
+}
+
+// 30-bit split accumulators: for a, b < 2^60 the product is
+//   a0 b0 + (a0 b1 + a1 b0) 2^30 + a1 b1 2^60,  pieces < 2^30.
+// Up to 8 products accumulate without overflow (mid term: 16 partials < 2^64).
+struct Acc3 {
+  u64 lo, mid, hi;
+};
+CK_D void acc3_zero(Acc3& s) { s.lo = s.mid = s.hi = 0; }
+CK_D void acc3_mac(Acc3& s, u32 a0, u32 a1, u32 b0, u32 b1) {
+  s.lo += (u64)a0 * b0;
+  s.mid += (u64)a0 * b1;
+  s.mid += (u64)a1 * b0;
+  s.hi += (u64)a1 * b1;
+}
+CK_D u32 lo30(u64 x) { return (u32)x & 0x3fffffffu; }
+CK_D u32 hi30(u64 x) { return (u32)(x >> 30); }
+
+// Reduce lo + mid*2^30 + hi*2^60 into [0, q).
+CK_D u64 acc3_reduce(const Acc3& s, const PrimeConst& P) {
+  u64 r = red64_lazy(s.lo, P) + shoup_lazy(s.mid, P.c30, P.c30p, P.q) +
+          shoup_lazy(s.hi, P.c60, P.c60p, P.q);  // < 6q
+  r = csub(r, P.two_q << 1);
+  r = csub(r, P.two_q);
+  return csub(r, P.q);
+}
+
+// ---- NTT butterflies (Harvey lazy) ----
+// Forward CT: X, Y in [0, 4q) -> [0, 4q).
+CK_D void bfly_ct(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
+  u64 x = csub(X, two_q);
+  u64 t = shoup_lazy(Y, w, wp, q);
+  X = x + t;
+  Y = x - t + two_q;
+}
+// Inverse GS: X, Y in [0, 2q) -> [0, 2q).
+CK_D void bfly_gs(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
+  u64 x = X, y = Y;
+  X = csub(x + y, two_q);
+  Y = shoup_lazy(x - y + two_q, w, wp, q);
+}
+
+// ---- index helpers ----
+CK_D u32 brev_bits(u32 x, int bits) { return bits ? (__brev(x) >> (32 - bits)) : 0u; }
+
+// Eval-domain Galois gather: out[i] = in[perm(i)],
+// perm(i) = br(((t * (2 br(i) + 1)) mod 2N - 1) / 2)   (rnspoly.py:127-135).
+CK_D u32 automorph_src(u32 i, u32 t, int logn) {
+  u32 j = brev_bits(i, logn);
+  u32 e = (u32)(((u64)t * (2u * j + 1u)) & ((2ull << logn) - 1));
+  return brev_bits((e - 1u) >> 1, logn);
+}

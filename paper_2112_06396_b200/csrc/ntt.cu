@@ -1,0 +1,223 @@
+// NTT / INTT kernels (see ntt.cuh for the decomposition).
+#include "ntt.cuh"
+#include "ck_internal.h"
+
+namespace ck {
+
+CK_D long long job_offset(const NttArgs& a, int job) {
+  return (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) +
+         (long long)blockIdx.z * a.batch_stride;
+}
+
+// ------------------------------------------------------------ column phase
+// grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
+template <int P1, int P2, bool INV>
+__global__ void __launch_bounds__(kTC * (1 << P1) / kE)
+ntt_col_kernel(NttArgs a) {
+  constexpr int S = 1 << P1;
+  constexpr int G = S / kE;
+  constexpr int NP = Sched<P1>::np;
+  __shared__ u64 sm[S * kTC];
+  __shared__ ulonglong2 tws[S];
+  const int job = blockIdx.y;
+  const int prime = a.prime_idx[job];
+  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
+  const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
+  for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
+  u64* base = a.data + job_offset(a, job);
+  const int col = threadIdx.x % kTC, g = threadIdx.x / kTC;
+  const int c = blockIdx.x * kTC + col;
+  u64 x[kE];
+#pragma unroll
+  for (int r = 0; r < kE; ++r) x[r] = base[((long long)sub_index<P1, 0, INV>(g, r) << P2) + c];
+  __syncthreads();
+  run_pass<P1, 0, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+  if constexpr (NP > 1) {
+#pragma unroll
+    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 0, INV>(g, r) * kTC + col] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 1, INV>(g, r) * kTC + col];
+    run_pass<P1, 1, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+  }
+  if constexpr (NP > 2) {
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 1, INV>(g, r) * kTC + col] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 2, INV>(g, r) * kTC + col];
+    run_pass<P1, 2, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+  }
+  static_assert(NP <= 3, "sub-transform too large");
+  if (INV) {
+    // end of the inverse: scale by n^-1 (times the optional extra constant)
+    const ulonglong2 s = a.scale ? a.scale[job]
+                                 : make_ulonglong2(a.pc[prime].ninv, a.pc[prime].ninvp);
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = shoup(x[r], s.x, s.y, q);
+  }
+  // forward: values stay lazy in [0,4q) for the row phase
+#pragma unroll
+  for (int r = 0; r < kE; ++r)
+    base[((long long)sub_index<P1, NP - 1, INV>(g, r) << P2) + c] = x[r];
+}
+
+// --------------------------------------------------------------- row phase
+// grid = (2^P1 / TR, jobs, batch); block = TR * 2^P2 / kE
+template <int P2>
+struct RowCfg {
+  static constexpr int S = 1 << P2;
+  static constexpr int G = S / kE;
+  static constexpr int TR = 256 / G > 0 ? 256 / G : 1;
+  static constexpr int RS = S + S / 16;  // padded smem row stride
+};
+
+template <int P1, int P2, bool INV>
+__global__ void __launch_bounds__(256)
+ntt_row_kernel(NttArgs a) {
+  using R = RowCfg<P2>;
+  constexpr int NP = Sched<P2>::np;
+  __shared__ u64 sm[R::TR * R::RS];
+  const int job = blockIdx.y;
+  const int prime = a.prime_idx[job];
+  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
+  const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
+  u64* base = a.data + job_offset(a, job);
+  const int rl = threadIdx.x / R::G, g = threadIdx.x % R::G;
+  const int row = blockIdx.x * R::TR + rl;
+  u64* rowp = base + ((long long)row << P2);
+  u64* srow = sm + rl * R::RS;
+  const int jbase = row << P2;
+  u64 x[kE];
+  auto sidx = [](int s) { return s + (s >> 4); };
+  if (!INV) {
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = rowp[sub_index<P2, 0, INV>(g, r)];
+  } else {
+    // pass 0 of the inverse reads contiguous runs: stage through smem
+    u64* tile = base + ((long long)blockIdx.x * R::TR << P2);
+    for (int i = threadIdx.x; i < R::TR * R::S; i += blockDim.x)
+      sm[(i >> P2) * R::RS + sidx(i & (R::S - 1))] = tile[i];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 0, INV>(g, r))];
+  }
+  run_pass<P2, 0, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+  if constexpr (NP > 1) {
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, 0, INV>(g, r))] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 1, INV>(g, r))];
+    run_pass<P2, 1, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+  }
+  if constexpr (NP > 2) {
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, 1, INV>(g, r))] = x[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 2, INV>(g, r))];
+    run_pass<P2, 2, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+  }
+  static_assert(NP <= 3, "sub-transform too large");
+  if (!INV) {
+    // end of the forward transform: canonical residues; stores staged
+    // through smem so the global writes are coalesced
+#pragma unroll
+    for (int r = 0; r < kE; ++r) x[r] = csub(csub(x[r], two_q), q);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, NP - 1, INV>(g, r))] = x[r];
+    __syncthreads();
+    u64* tile = base + ((long long)blockIdx.x * R::TR << P2);
+    for (int i = threadIdx.x; i < R::TR * R::S; i += blockDim.x)
+      tile[i] = sm[(i >> P2) * R::RS + sidx(i & (R::S - 1))];
+  } else {
+#pragma unroll
+    for (int r = 0; r < kE; ++r) rowp[sub_index<P2, NP - 1, INV>(g, r)] = x[r];
+  }
+}
+
+// ------------------------------------------------------- small N (<= 2^11)
+// One CTA per limb; plain radix-2 stages in shared memory.
+template <bool INV>
+__global__ void __launch_bounds__(512) ntt_small_kernel(NttArgs a) {
+  extern __shared__ u64 sx[];
+  const int n = 1 << a.logn;
+  const int job = blockIdx.y;
+  const int prime = a.prime_idx[job];
+  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
+  const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
+  u64* base = a.data + job_offset(a, job);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = base[i];
+  __syncthreads();
+  if (!INV) {
+    for (int logt = a.logn - 1; logt >= 0; --logt) {
+      const int t = 1 << logt, m = n >> (logt + 1);
+      for (int b = threadIdx.x; b < n / 2; b += blockDim.x) {
+        const int blk = b >> logt, off = b & (t - 1);
+        const int j = (blk << (logt + 1)) + off;
+        const ulonglong2 w = tw[m + blk];
+        bfly_ct(sx[j], sx[j + t], w.x, w.y, q, two_q);
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) base[i] = csub(csub(sx[i], two_q), q);
+  } else {
+    for (int logt = 0; logt < a.logn; ++logt) {
+      const int t = 1 << logt, h = n >> (logt + 1);
+      for (int b = threadIdx.x; b < n / 2; b += blockDim.x) {
+        const int blk = b >> logt, off = b & (t - 1);
+        const int j = (blk << (logt + 1)) + off;
+        const ulonglong2 w = tw[h + blk];
+        bfly_gs(sx[j], sx[j + t], w.x, w.y, q, two_q);
+      }
+      __syncthreads();
+    }
+    const ulonglong2 s = a.scale ? a.scale[job]
+                                 : make_ulonglong2(a.pc[prime].ninv, a.pc[prime].ninvp);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) base[i] = shoup(sx[i], s.x, s.y, q);
+  }
+}
+
+// ------------------------------------------------------------------ launch
+template <int P1, int P2>
+static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, cudaStream_t st) {
+  const dim3 gcol((1 << P2) / kTC, jobs, batch), bcol(kTC * (1 << P1) / kE);
+  using R = RowCfg<P2>;
+  const dim3 grow((1 << P1) / R::TR, jobs, batch), brow(R::TR * R::G);
+  count_launches(2);
+  if (!inv) {
+    ntt_col_kernel<P1, P2, false><<<gcol, bcol, 0, st>>>(a);
+    ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
+  } else {
+    ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
+    ntt_col_kernel<P1, P2, true><<<gcol, bcol, 0, st>>>(a);
+  }
+}
+
+int launch_ntt(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st) {
+  if (jobs <= 0 || batch <= 0) return 0;
+  switch (a.logn) {
+    case 12: launch_split<6, 6>(a, jobs, batch, inverse, st); break;
+    case 13: launch_split<6, 7>(a, jobs, batch, inverse, st); break;
+    case 14: launch_split<7, 7>(a, jobs, batch, inverse, st); break;
+    case 15: launch_split<7, 8>(a, jobs, batch, inverse, st); break;
+    case 16: launch_split<8, 8>(a, jobs, batch, inverse, st); break;
+    case 17: launch_split<8, 9>(a, jobs, batch, inverse, st); break;
+    default: {
+      if (a.logn < 1 || a.logn > 11) return CK_ERR_ARG;
+      const int n = 1 << a.logn;
+      count_launches(1);
+      const dim3 grid(1, jobs, batch), blk(n / 2 < 512 ? (n / 2 > 0 ? n / 2 : 1) : 512);
+      if (inverse) ntt_small_kernel<true><<<grid, blk, n * sizeof(u64), st>>>(a);
+      else ntt_small_kernel<false><<<grid, blk, n * sizeof(u64), st>>>(a);
+    }
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace ck

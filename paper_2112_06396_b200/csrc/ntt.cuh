@@ -1,0 +1,98 @@
+// Negacyclic NTT / INTT for one RNS limb row of N = 2^logn uint64 residues.
+//
+// Semantics are those of the reference NttContext (rnspoly.py:48-79):
+// forward = Cooley-Tukey DIT with bit-reversed twiddles tw[m + block]
+// (natural in, bit-reversed out); inverse = Gentleman-Sande ladder with
+// itw[h + block], then * n^-1 (here: * a per-row scale, n^-1 times an
+// optional extra constant such as the ModUp/ModDown ihat, folded exactly).
+//
+// B200 layout: a limb (512 KB at N=2^16) does not fit one SM, so the
+// transform is split as N = 2^P1 x 2^P2 over the storage matrix
+// x[r * 2^P2 + c]:
+//   * column phase: stages with m < 2^P1 only mix rows of one column
+//     (twiddles tw[1 .. 2^P1) shared by all columns, staged in SMEM);
+//   * row phase: stages with m >= 2^P1 only mix a contiguous row of 2^P2
+//     elements (twiddles for that row read through L1/L2).
+// Inside a phase each thread keeps E = 16 elements in registers and runs up
+// to 4 radix-2 stages on them (a radix-16 pass); passes exchange through
+// shared memory.  Arithmetic: 64-bit Shoup/Harvey lazy butterflies
+// (modarith.cuh), values in [0,4q) between stages, canonical on output.
+#pragma once
+#include "modarith.cuh"
+
+namespace ck {
+
+constexpr int kElog = 4;
+constexpr int kE = 1 << kElog;  // elements per thread
+constexpr int kTC = 16;         // columns per column-phase CTA (128 B rows)
+
+struct NttArgs {
+  u64* data;
+  const int* prime_idx;        // per job: index into the plan's prime table
+  const long long* row_off;    // per job: element offset of the limb (nullable: job*N)
+  const PrimeConst* pc;
+  const ulonglong2* tw;        // [prime][N] {w, w_shoup}, forward
+  const ulonglong2* itw;       // [prime][N] inverse
+  const ulonglong2* scale;     // per job {s, s_shoup} applied after INTT (nullable: n^-1)
+  long long batch_stride;      // elements between batch items (grid.z)
+  int logn;
+};
+
+// ---- compile-time pass schedule for a 2^P-point sub-transform ----
+template <int P>
+struct Sched {
+  static constexpr int np = (P + kElog - 1) / kElog;
+  static constexpr int C(int p) { return p < np - 1 ? kElog : P - kElog * (np - 1); }
+  static constexpr int sumC(int p) { return p < 0 ? 0 : C(p) + sumC(p - 1); }
+  // log2 of the smallest in-pass distance
+  static constexpr int logD(int p, bool inv) { return inv ? sumC(p - 1) : P - sumC(p); }
+};
+
+// Sub-index (within the 2^P-point sub-transform) of register r of thread g.
+template <int P, int p, bool INV>
+CK_D int sub_index(int g, int r) {
+  constexpr int C = Sched<P>::C(p);
+  constexpr int LD = Sched<P>::logD(p, INV);
+  constexpr int NG = kE >> C;
+  const int h = r >> C, k = r & ((1 << C) - 1);
+  const int gamma = g * NG + h;
+  const int blk = gamma >> LD, lo = gamma & ((1 << LD) - 1);
+  return (blk << (LD + C)) + lo + (k << LD);
+}
+
+// One register pass.  j(s) = jbase + (s << jshift) is the limb-global index.
+template <int P, int p, bool INV, bool TW_SMEM>
+CK_D void run_pass(u64 (&x)[kE], int g, int jbase, int jshift, int logn,
+                   const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
+  constexpr int C = Sched<P>::C(p);
+  constexpr int LD = Sched<P>::logD(p, INV);
+  constexpr int NG = kE >> C;
+#pragma unroll
+  for (int h = 0; h < NG; ++h) {
+    const int s0 = sub_index<P, p, INV>(g, h << C);
+#pragma unroll
+    for (int st = 0; st < C; ++st) {
+      // forward: distances shrink (half = 2^(C-1-st)); inverse: grow (2^st)
+      const int lhalf = INV ? st : (C - 1 - st);
+      const int half = 1 << lhalf;
+      const int logt = LD + lhalf + jshift;  // log2 of limb-global distance
+      const int logm = logn - 1 - logt;      // stage m (fwd) or h (inv)
+#pragma unroll
+      for (int b = 0; b < (1 << C) / (2 * half); ++b) {
+        const int k0 = b * 2 * half;
+        const int j = jbase + ((s0 + (k0 << LD)) << jshift);
+        const int idx = (1 << logm) + (j >> (logt + 1));
+        ulonglong2 w;
+        if (TW_SMEM) w = tw[idx];
+        else w = __ldg(tw + idx);
+#pragma unroll
+        for (int k = k0; k < k0 + half; ++k) {
+          if (INV) bfly_gs(x[(h << C) + k], x[(h << C) + k + half], w.x, w.y, q, two_q);
+          else bfly_ct(x[(h << C) + k], x[(h << C) + k + half], w.x, w.y, q, two_q);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace ck
