@@ -623,7 +623,7 @@ int ck_automorph(const ck_plan* p, uint64_t* out_, const uint64_t* x_, int rows,
   if (!p || !out || !x || rows < 0 || (galois_t & 1) == 0) return CK_ERR_ARG;
   if (rows == 0) return 0;
   return ew_run(p, ck::EW_AUTOMORPH, out, 0, x, 0, nullptr, 0, nullptr, 0, nullptr, nullptr,
-                galois_t % (2ull * p->n), nullptr, 1, rows, (cudaStream_t)stream);
+                galois_t % (2ull * p->n), nullptr, rows, 1, (cudaStream_t)stream);
 }
 
 int ck_bconv_create(const ck_plan* p, const int32_t* src_idx, int ns, const int32_t* dst_idx,
