@@ -9,9 +9,14 @@
 //   y_j  -= k * Q mod p_j                        (centered only)
 //
 // The sum is an exact integer reduced mod p_j, so any exact accumulation
-// matches the reference.  Here it is a small modular contraction on CUDA
-// cores with 30-bit split operands: four 32x32->64 IMAD.WIDE per term into
-// three 64-bit accumulators, one reduction per (coefficient, target).
+// matches the reference.  It is a small modular contraction on CUDA cores
+// (IMAD.WIDE is half-rate on sm_100, 32-bit IMAD full rate; measured in
+// profiles/r01_microbench_int.txt), arranged to need only TWO 64-bit
+// accumulators and one 2-step reduction per (coefficient, target):
+//   v = v0 + v1 2^30 (30-bit pieces), T = t0 + t1 2^30, U = T 2^30 mod p = u0 + u1 2^30
+//   v T == (v0 t0 + v1 u0) + (v0 t1 + v1 u1) 2^30   (mod p)
+// Each 30x30-bit partial product is < 2^60, so up to 8 sources (16 partials
+// per accumulator) accumulate without overflow; more sources are chunked.
 // The float estimate replicates numpy's op order with explicit _rn
 // intrinsics (no FMA contraction), round-half-even via rint().
 #include "ck_internal.h"
@@ -19,79 +24,125 @@
 namespace ck {
 
 constexpr int kBcThreads = 128;
+constexpr int kBcCpt = 2;  // coefficients per thread
 
-template <int MAXS>
+struct BcDst {
+  u64 p, bar, c30, c30p;
+};
+
+template <int NS>
 __global__ void __launch_bounds__(kBcThreads) bconv_kernel(BconvArgs a) {
-  __shared__ uint2 Ts[MAXS * 48];
-  const int ns = a.ns, nd = a.nd;
-  const bool tab_smem = ns * nd <= MAXS * 48;
-  if (tab_smem) {
-    for (int i = threadIdx.x; i < ns * nd; i += blockDim.x) {
-      const u64 t = a.T[i];
-      Ts[i] = make_uint2(lo30(t), hi30(t));
-    }
+  extern __shared__ __align__(16) unsigned char bc_smem[];
+  const int nd = a.nd;
+  uint4* Ts = (uint4*)bc_smem;                         // [NS][nd]
+  BcDst* Ds = (BcDst*)(Ts + NS * nd);                  // [nd]
+  u64* kQs = (u64*)(Ds + nd);                          // [nd][ns+1] (centered)
+  const int ns = a.ns;                                 // <= NS; rows >= ns are zero
+  for (int i = threadIdx.x; i < NS * nd; i += blockDim.x)
+    Ts[i] = i < ns * nd ? a.T[i] : make_uint4(0, 0, 0, 0);
+  for (int j = threadIdx.x; j < nd; j += blockDim.x) {
+    const PrimeConst& P = a.pc[a.dst_prime[j]];
+    Ds[j] = BcDst{P.q, P.bar, P.c30, P.c30p};
   }
+  if (a.centered)
+    for (int i = threadIdx.x; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
   __syncthreads();
+
   const int n = 1 << a.logn;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+  const int k0 = blockIdx.x * (kBcThreads * kBcCpt) + threadIdx.x;
   const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
   u64* out = a.out + (long long)blockIdx.z * a.out_batch;
 
-  u32 v0[MAXS], v1[MAXS];
-  double est = 0.0;
+  u32 v0[kBcCpt][NS], v1[kBcCpt][NS];
+  u32 kk[kBcCpt];
 #pragma unroll
-  for (int i = 0; i < MAXS; ++i) {
-    if (i < ns) {
-      const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
-      u64 v = in[off + k];
-      if (a.src_scale) {
-        const ulonglong2 s = a.src_scale[i];
-        v = shoup(v, s.x, s.y, a.pc[a.src_prime[i]].q);
+  for (int c = 0; c < kBcCpt; ++c) {
+    const int k = k0 + c * kBcThreads;
+    double est = 0.0;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      u64 v = 0;
+      if (i < ns) {
+        const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
+        v = k < n ? in[off + k] : 0;
+        if (a.src_scale) {
+          const ulonglong2 s = a.src_scale[i];
+          v = shoup(v, s.x, s.y, a.pc[a.src_prime[i]].q);
+        }
+        if (a.centered) est = __dadd_rn(est, __dmul_rn(__ull2double_rn(v), a.w[i]));
       }
-      if (a.centered) est = __dadd_rn(est, __dmul_rn(__ull2double_rn(v), a.w[i]));
-      v0[i] = lo30(v);
-      v1[i] = hi30(v);
+      v0[c][i] = lo30(v);
+      v1[c][i] = hi30(v);
     }
+    kk[c] = a.centered ? (u32)rint(est) : 0u;
   }
-  const u64 kk = a.centered ? (u64)rint(est) : 0;
 
   for (int j = 0; j < nd; ++j) {
-    const PrimeConst P = a.pc[a.dst_prime[j]];
-    u64 y = 0;
-    for (int i0 = 0; i0 < ns; i0 += 8) {
-      Acc3 s;
-      acc3_zero(s);
+    const BcDst D = Ds[j];
+    u64 y[kBcCpt], lo[kBcCpt], hi[kBcCpt];
 #pragma unroll
-      for (int ii = 0; ii < 8; ++ii) {
-        const int i = i0 + ii;
-        if (i < ns && i < MAXS) {
-          uint2 t;
-          if (tab_smem) t = Ts[i * nd + j];
-          else {
-            const u64 tt = a.T[i * nd + j];
-            t = make_uint2(lo30(tt), hi30(tt));
-          }
-          acc3_mac(s, v0[i], v1[i], t.x, t.y);
+    for (int c = 0; c < kBcCpt; ++c) y[c] = lo[c] = hi[c] = 0;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      const uint4 t = Ts[i * nd + j];
+#pragma unroll
+      for (int c = 0; c < kBcCpt; ++c) {
+        lo[c] += (u64)v0[c][i] * t.x;
+        lo[c] += (u64)v1[c][i] * t.z;
+        hi[c] += (u64)v0[c][i] * t.y;
+        hi[c] += (u64)v1[c][i] * t.w;
+      }
+      if ((i & 7) == 7 || i == NS - 1) {  // chunk of <= 8 sources: reduce
+#pragma unroll
+        for (int c = 0; c < kBcCpt; ++c) {
+          // lo + hi 2^30 mod p, each piece lazily in [0, 2p)
+          u64 r = (lo[c] - mulhi64(lo[c], D.bar) * D.p) + shoup_lazy(hi[c], D.c30, D.c30p, D.p);
+          r = csub(r, 2 * D.p);
+          r = csub(r, D.p);
+          y[c] = i < 8 ? r : addmod(y[c], r, D.p);
+          lo[c] = hi[c] = 0;
         }
       }
-      y = addmod(y, acc3_reduce(s, P), P.q);
     }
-    if (a.centered) y = submod(y, a.kQ[j * (ns + 1) + kk], P.q);
     const long long off = a.out_off ? a.out_off[j] : ((long long)j << a.logn);
-    out[off + k] = y;
+#pragma unroll
+    for (int c = 0; c < kBcCpt; ++c) {
+      const int k = k0 + c * kBcThreads;
+      u64 r = y[c];
+      if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[c]], D.p);
+      if (k < n) out[off + k] = r;
+    }
   }
+}
+
+template <int NS>
+static void launch_ns(const BconvArgs& a, int batch, cudaStream_t st) {
+  const int n = 1 << a.logn;
+  const int per = kBcThreads * kBcCpt;
+  const dim3 grid((n + per - 1) / per, 1, batch);
+  const size_t smem = (size_t)NS * a.nd * sizeof(uint4) + a.nd * sizeof(BcDst) +
+                      (a.centered ? (size_t)a.nd * (a.ns + 1) * sizeof(u64) : 0);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(bconv_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bconv_kernel<NS><<<grid, kBcThreads, smem, st>>>(a);
 }
 
 int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st) {
   if (a.nd <= 0 || batch <= 0) return 0;
-  if (a.ns <= 0) return CK_ERR_ARG;
-  const int n = 1 << a.logn;
-  const dim3 grid((n + kBcThreads - 1) / kBcThreads, 1, batch);
   count_launches(1);
-  if (a.ns <= 8) bconv_kernel<8><<<grid, kBcThreads, 0, st>>>(a);
-  else if (a.ns <= 16) bconv_kernel<16><<<grid, kBcThreads, 0, st>>>(a);
-  else if (a.ns <= 64) bconv_kernel<64><<<grid, kBcThreads, 0, st>>>(a);
+  // smallest compiled source count >= ns (extra source rows are zero)
+  if (a.ns < 1) return CK_ERR_ARG;
+  if (a.ns <= 1) launch_ns<1>(a, batch, st);
+  else if (a.ns <= 2) launch_ns<2>(a, batch, st);
+  else if (a.ns <= 4) launch_ns<4>(a, batch, st);
+  else if (a.ns <= 8) launch_ns<8>(a, batch, st);
+  else if (a.ns <= 9) launch_ns<9>(a, batch, st);
+  else if (a.ns <= 10) launch_ns<10>(a, batch, st);
+  else if (a.ns <= 12) launch_ns<12>(a, batch, st);
+  else if (a.ns <= 16) launch_ns<16>(a, batch, st);
+  else if (a.ns <= 24) launch_ns<24>(a, batch, st);
+  else if (a.ns <= 32) launch_ns<32>(a, batch, st);
+  else if (a.ns <= 48) launch_ns<48>(a, batch, st);
   else return CK_ERR_ARG;
   return (int)cudaGetLastError();
 }

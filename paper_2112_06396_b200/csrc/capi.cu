@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -103,7 +104,7 @@ struct ck_bconv {
   int* d_src = nullptr;
   int* d_dst = nullptr;
   ulonglong2* d_ihat = nullptr;   // plain ihat (generic apply)
-  u64* d_T = nullptr;
+  uint4* d_T = nullptr;
   double* d_w = nullptr;
   u64* d_kQ = nullptr;
   long long* d_out_off = nullptr; // optional
@@ -144,6 +145,7 @@ struct LevelTab {
 
 struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
+  bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   ulonglong2* d_tw = nullptr;
@@ -196,7 +198,7 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
   b->nd = (int)dst.size();
   b->centered = centered;
   std::vector<ulonglong2> ihat(src.size());
-  std::vector<u64> T(src.size() * dst.size());
+  std::vector<uint4> T(src.size() * dst.size());
   std::vector<double> w(src.size());
   for (size_t i = 0; i < src.size(); ++i) {
     const u64 qi = p->mod[src[i]];
@@ -209,7 +211,10 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
       u64 t = 1 % pj;
       for (size_t k = 0; k < src.size(); ++k)
         if (k != i) t = mulmod_h(t, p->mod[src[k]] % pj, pj);
-      T[i * dst.size() + j] = t;
+      // 30-bit pieces of T and of U = T * 2^30 mod p (bconv.cu: two accumulators)
+      const u64 u = mulmod_h(t, (u64)1 << 30, pj);
+      const u32 m30 = (1u << 30) - 1;
+      T[i * dst.size() + j] = make_uint4((u32)t & m30, (u32)(t >> 30), (u32)u & m30, (u32)(u >> 30));
     }
     w[i] = 1.0 / (double)qi;  // Python: 1.0 / q  (q rounded to double first)
   }
@@ -348,6 +353,22 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
 
+int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* off,
+              const ulonglong2* scale, int jobs, int batch, long long bstride, bool inv,
+              int phase, cudaStream_t st) {
+  ck::NttArgs a;
+  a.data = base;
+  a.prime_idx = prime;
+  a.row_off = off;
+  a.pc = p->d_pc;
+  a.tw = p->d_tw;
+  a.itw = p->d_itw;
+  a.scale = scale;
+  a.batch_stride = bstride;
+  a.logn = p->logn;
+  return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
+}
+
 int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
               u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st) {
   ck::BconvArgs a;
@@ -478,6 +499,88 @@ int moddown_core(const ck_plan* p, const ModDownTab& m, u64* x, long long xb, u6
                   false, st);
 }
 
+// Fused rotation key-switch (see fused.cu); 10 + beta launches per batch.
+int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add,
+                 const u64* kb, const u64* ka, u64 kgt, const u64* kgal, u64 egt,
+                 const u64* egal, u64* out_a, u64* out_b, const Ws& w, int B, cudaStream_t st) {
+  const LevelTab& t = p->lv[level];
+  const ModDownTab& m = t.md[0];
+  const long long N = p->n, l = level, R = t.R;
+  const long long dig_b = (long long)t.beta * R * N;
+  // ---- ModUp: INTT of a (row then column phase, ihat*n^-1 folded), BC, fwd column phase
+  CK_TRY((int)cudaMemcpyAsync(w.tmp, a_src, sizeof(u64) * B * l * N, cudaMemcpyDeviceToDevice, st));
+  CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, nullptr, level, B, l * N, true, 2, st));
+  CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, t.d_modup_scale, level, B, l * N, true, 1,
+                   st));
+  for (int d = 0; d < t.beta; ++d)
+    CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
+                     false, B, st));
+  CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
+                   dig_b, false, 1, st));
+  // ---- row phase + automorph + KSKIP (+ INTT row phase of the special rows)
+  ck::KsRowArgs ka_;
+  ka_.a_eval = a_src;
+  ka_.a_batch = l * N;
+  ka_.dig = w.dig;
+  ka_.dig_batch = dig_b;
+  ka_.key_b = kb;
+  ka_.key_a = ka;
+  ka_.key_digit_stride = (long long)(p->L + p->K) * N;
+  ka_.key_batch = (long long)p->key_digits * (p->L + p->K) * N;
+  ka_.uv = w.uv;
+  ka_.uv_batch = 2 * R * N;
+  ka_.v_off = R * N;
+  ka_.prime = t.d_raised_prime;
+  ka_.pc = p->d_pc;
+  ka_.tw = p->d_tw;
+  ka_.itw = p->d_itw;
+  ka_.galois = kgal;
+  ka_.galois_t = kgt;
+  for (int d = 0; d < 16; ++d) {
+    ka_.lo[d] = d < t.beta ? t.lo[d] : 0;
+    ka_.hi[d] = d < t.beta ? t.hi[d] : 0;
+  }
+  ka_.beta = t.beta;
+  ka_.l = level;
+  ka_.R = (int)R;
+  ka_.logn = p->logn;
+  ka_.intt_special = 1;
+  CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
+  // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
+  CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
+                   true, 1, st));
+  CK_TRY(bconv_run(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv, l * N, false, 2 * B,
+                   st));
+  CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false, 1,
+                   st));
+  // ---- fwd row phase of the converted rows fused with the epilogue
+  ck::MdRowArgs ma;
+  ma.prime = m.d_keep_prime;
+  ma.pinv = m.d_pinv;
+  ma.pc = p->d_pc;
+  ma.tw = p->d_tw;
+  ma.logn = p->logn;
+  ma.x = w.uv;
+  ma.x_batch = 2 * R * N;
+  ma.conv = w.conv;
+  ma.conv_batch = 2 * l * N;
+  ma.addend = nullptr;
+  ma.addend_batch = 0;
+  ma.out = out_a;
+  ma.out_batch = l * N;
+  ma.galois = nullptr;
+  ma.galois_t = 1;
+  CK_TRY(ck::launch_md_row(ma, level, B, st));
+  ma.x = w.uv + R * N;
+  ma.conv = w.conv + l * N;
+  ma.addend = b_add;
+  ma.addend_batch = l * N;
+  ma.out = out_b;
+  ma.galois = egal;
+  ma.galois_t = egt;
+  return ck::launch_md_row(ma, level, B, st);
+}
+
 }  // namespace
 
 // ==================================================================== C ABI
@@ -513,6 +616,10 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   p->dnum = dnum;
   p->alpha = (n_chain + dnum - 1) / dnum;
   p->key_digits = (n_chain + p->alpha - 1) / p->alpha;
+  {
+    const char* e = getenv("CKB200_UNFUSED");
+    p->fused = !(e && e[0] == '1');
+  }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
   const u64 two_n = 2ull << log_n;
@@ -738,6 +845,9 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
     egt = 1;
     kgal = nullptr;
   }
+  if (ck::fused_supported(p->logn) && p->fused)
+    return rotate_fused(p, level, a_src, b_add, key_b, key_a, kgt, kgal, egt,
+                        mode == 1 ? nullptr : galois, out_a, out_b, w, batch, st);
   CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
   // uv: [B][2][R][N]
   CK_TRY(kskip_impl(p, level, w.dig, key_b, key_a, kgt, kgal, w.uv, w.uv + R * N, 2 * R * N,

@@ -20,6 +20,50 @@ void count_launches(int n);
 
 struct NttArgs;
 int launch_ntt(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st);
+int launch_ntt_phase(const NttArgs& a, int jobs, int batch, bool inverse, int phase,
+                     cudaStream_t st);
+bool fused_supported(int logn);
+
+// Fused row kernels (fused.cu)
+struct KsRowArgs {
+  const u64* a_eval;            // [B][l][N] eval input (own digit rows)
+  long long a_batch;
+  const u64* dig;               // [B][beta][R][N] ModUp targets after the column phase
+  long long dig_batch;
+  const u64* key_b;
+  const u64* key_a;
+  long long key_digit_stride, key_batch;
+  u64* uv;                      // u at uv + i*N, v at uv + v_off + i*N (per batch item)
+  long long uv_batch, v_off;
+  const int* prime;             // [R] raised prime index (== full-basis key row)
+  const PrimeConst* pc;
+  const ulonglong2* tw;
+  const ulonglong2* itw;
+  const u64* galois;            // per batch item (nullable: galois_t)
+  u64 galois_t;
+  int lo[16], hi[16];           // digit spans (chain rows)
+  int beta, l, R, logn, intt_special;
+};
+int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
+
+struct MdRowArgs {
+  const u64* x;                 // [B][..][N] raised-basis rows (kept rows j = 0..keep)
+  long long x_batch;
+  const u64* conv;              // [B][keep][N] converted rows after the column phase
+  long long conv_batch;
+  const u64* addend;            // nullable [B][keep][N], gathered with galois
+  long long addend_batch;
+  u64* out;
+  long long out_batch;
+  const int* prime;             // [keep]
+  const ulonglong2* pinv;       // [keep]
+  const PrimeConst* pc;
+  const ulonglong2* tw;
+  const u64* galois;
+  u64 galois_t;
+  int logn;
+};
+int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st);
 
 // Basis conversion: ns source rows (coefficient rep, same coefficient index)
 // -> nd destination rows.  T[i*nd+j] = (Q/q_i) mod p_j.
@@ -34,7 +78,7 @@ struct BconvArgs {
   const int* dst_prime;         // [nd]
   const PrimeConst* pc;
   const ulonglong2* src_scale;  // [ns] ihat Shoup pairs; nullable = already scaled
-  const u64* T;                 // [ns*nd]
+  const uint4* T;               // [ns*nd] {t0,t1,u0,u1}: T = t0+t1 2^30, T 2^30 mod p = u0+u1 2^30
   const double* w;              // [ns] 1.0/q_i   (centered only)
   const u64* kQ;                // [nd*(ns+1)] k*Q mod p_j  (centered only)
   int ns, nd, logn, centered;

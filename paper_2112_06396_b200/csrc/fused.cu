@@ -1,0 +1,256 @@
+// Fused key-switch row kernels (the NTT's row phase + what follows it).
+//
+// ks_row_kernel: for raised limb i and a tile of storage rows r
+//   digit_d[i][r, :] = automorph( NTT_row( ModUp target row ) )   (or the
+//                      input a_eval row for the digit's own limbs,
+//                      ckks.py:433-440)
+//   u[i][r, :] = sum_d digit_d * key_a[d][row_i],  v likewise      (_kskip,
+//                      ckks.py:450-465, on automorph'ed digits, ckks.py:663)
+//   special limbs (i >= l): optionally run the INTT row phase on u, v right
+//   away -- the first half of ModDown's INTT (ckks.py:409).
+// The digits never touch HBM in evaluation form.  The automorphism maps a
+// storage row r to a single source row sigma(r) (see kskip.cu), so each CTA
+// loads whole source rows and gathers within shared memory.
+//
+// md_row_kernel: ModDown epilogue fused with the forward NTT row phase of the
+//   converted polynomial (ckks.py:410-416, 664-666):
+//   out[j][r, :] = (x[j][r, :] - NTT_row(conv[j])[r, :]) * P^-1 [+ automorph(b)]
+#include "ck_internal.h"
+#include "ntt.cuh"
+
+namespace ck {
+
+template <int P2>
+struct FusedCfg {
+  static constexpr int S = 1 << P2;
+  static constexpr int G = S / kE;         // threads per row
+  static constexpr int TR = 2048 / S;      // rows per CTA (2048 elements)
+  static constexpr int NT = TR * G;        // 128 threads
+  static constexpr int RS = row_stride<P2>();
+};
+
+// ---------------------------------------------------------------- KSKIP row
+// BETA > 0: compile-time digit count (fully unrolled inner product, so the
+// 2*BETA key loads of an element are independent and stay in flight);
+// BETA == 0: runtime a.beta (generic fallback).
+template <int P1, int P2, int BETA>
+__global__ void __launch_bounds__(FusedCfg<P2>::NT) ks_row_kernel(KsRowArgs a) {
+  using F = FusedCfg<P2>;
+  constexpr int LOGN = P1 + P2;
+  extern __shared__ __align__(16) u64 fsm[];
+  u64* stage = fsm;                     // [TR][RS] exchange / staging
+  u64* dsm = fsm + F::TR * F::RS;       // [beta][TR * S] gathered digits (MAC layout)
+  const int i = blockIdx.y;
+  const long long b = blockIdx.z;
+  const int prime = a.prime[i];
+  const PrimeConst& P = a.pc[prime];
+  const u64 q = P.q, two_q = P.two_q;
+  const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
+  const int r = blockIdx.x * F::TR + rl;
+  u64* srow = stage + rl * F::RS;
+  const u64 t = a.galois ? a.galois[b] : a.galois_t;
+  const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
+  const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
+
+#pragma unroll 1
+  for (int d = 0; d < a.beta; ++d) {
+    const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
+    u64 x[kE];
+    if (own) {
+      const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
+#pragma unroll
+      for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
+      __syncthreads();
+      row_to_smem<P2, 0, false>(x, g, srow);
+    } else {
+      const u64* src = a.dig + b * a.dig_batch + ((long long)(d * a.R + i) << LOGN) +
+                       ((long long)sr << P2);
+#pragma unroll
+      for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
+      row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
+#pragma unroll
+      for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+      __syncthreads();
+      row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+    }
+    __syncthreads();
+    // gather: output column c of row r reads column pi_r(c) of row sigma(r)
+    u64* dd = dsm + (long long)d * (F::TR * F::S) + rl * F::S;
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const int c = sub_index<P2, 0, false>(g, k);
+      const int sc = t == 1 ? c
+                            : (int)(automorph_src(((u32)r << P2) + c, (u32)t, LOGN) & (F::S - 1));
+      dd[c] = srow[sidx(sc)];
+    }
+  }
+
+  // inner product with the key rows (coalesced: MAC layout = pass-0 layout)
+  const int krow = prime;
+  const u64* ka = a.key_a + b * a.key_batch + ((long long)krow << LOGN) + ((long long)r << P2);
+  const u64* kb = a.key_b + b * a.key_batch + ((long long)krow << LOGN) + ((long long)r << P2);
+  u64* uo = a.uv + b * a.uv_batch + ((long long)i << LOGN) + ((long long)r << P2);
+  u64* vo = uo + a.v_off;
+  const bool inv_now = a.intt_special && i >= a.l;
+  u64* du = dsm + rl * F::S;                 // reused: u (digit slot 0), v (slot 1)
+  u64* dv = dsm + (F::TR * F::S) + rl * F::S;
+  constexpr int NB = BETA > 0 ? BETA : 8;
+  const int beta = BETA > 0 ? BETA : a.beta;
+#pragma unroll 4
+  for (int k = 0; k < kE; ++k) {
+    const int c = sub_index<P2, 0, false>(g, k);
+    Acc3 su, sv;
+    acc3_zero(su);
+    acc3_zero(sv);
+#pragma unroll
+    for (int d = 0; d < NB; ++d) {
+      if (BETA == 0 && d >= beta) break;
+      const u64 x = dsm[(long long)d * (F::TR * F::S) + rl * F::S + c];
+      const u64 ya = __ldg(ka + d * a.key_digit_stride + c);
+      const u64 yb = __ldg(kb + d * a.key_digit_stride + c);
+      const u32 x0 = lo30(x), x1 = hi30(x);
+      acc3_mac(su, x0, x1, lo30(ya), hi30(ya));
+      acc3_mac(sv, x0, x1, lo30(yb), hi30(yb));
+    }
+    const u64 uu = acc3_reduce(su, P), vv = acc3_reduce(sv, P);
+    if (inv_now) {
+      du[c] = uu;  // thread-private slots: every digit value at c is consumed
+      dv[c] = vv;
+    } else {
+      uo[c] = uu;
+      vo[c] = vv;
+    }
+  }
+  if (inv_now) {
+    // first half of ModDown's INTT: inverse row phase, output lazy [0, 2q)
+    const ulonglong2* itw = a.itw + ((long long)prime << LOGN);
+    u64 y[kE];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kE; ++k) y[k] = du[sub_index<P2, 0, true>(g, k)];
+    row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
+#pragma unroll
+    for (int k = 0; k < kE; ++k) uo[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) y[k] = dv[sub_index<P2, 0, true>(g, k)];
+    row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
+#pragma unroll
+    for (int k = 0; k < kE; ++k) vo[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
+  }
+}
+
+// ------------------------------------------------------------ ModDown row
+template <int P1, int P2>
+__global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
+  using F = FusedCfg<P2>;
+  constexpr int LOGN = P1 + P2;
+  __shared__ u64 stage[F::TR * F::RS];
+  const int j = blockIdx.y;
+  const long long b = blockIdx.z;
+  const int prime = a.prime[j];
+  const PrimeConst& P = a.pc[prime];
+  const u64 q = P.q, two_q = P.two_q;
+  const ulonglong2 pinv = a.pinv[j];
+  const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
+  const int r = blockIdx.x * F::TR + rl;
+  u64* srow = stage + rl * F::RS;
+  const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
+  const long long ro = ((long long)j << LOGN) + ((long long)r << P2);
+  const u64* conv = a.conv + b * a.conv_batch + ro;
+  const u64* x = a.x + b * a.x_batch + ro;
+  u64 y[kE];
+#pragma unroll
+  for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
+  row_transform<P2, false, LOGN>(y, g, r << P2, srow, tw, q, two_q);
+#pragma unroll
+  for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
+  __syncthreads();
+  row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, srow);
+  __syncthreads();
+  u64 o[kE];
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const int c = sub_index<P2, 0, false>(g, k);
+    o[k] = shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
+  }
+  if (a.addend) {
+    const u64 t = a.galois ? a.galois[b] : a.galois_t;
+    const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
+    const u64* add = a.addend + b * a.addend_batch + ((long long)j << LOGN) + ((long long)sr << P2);
+    u64 z[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) z[k] = add[sub_index<P2, 0, false>(g, k)];
+    __syncthreads();
+    row_to_smem<P2, 0, false>(z, g, srow);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const int c = sub_index<P2, 0, false>(g, k);
+      const int sc = t == 1 ? c
+                            : (int)(automorph_src(((u32)r << P2) + c, (u32)t, LOGN) & (F::S - 1));
+      o[k] = addmod(o[k], srow[sidx(sc)], q);
+    }
+  }
+  u64* out = a.out + b * a.out_batch + ((long long)j << LOGN) + ((long long)r << P2);
+#pragma unroll
+  for (int k = 0; k < kE; ++k) out[sub_index<P2, 0, false>(g, k)] = o[k];
+}
+
+// ------------------------------------------------------------------ launch
+template <int P1, int P2>
+static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
+  using F = FusedCfg<P2>;
+  const int slots = a.beta < 2 ? 2 : a.beta;  // >= 2: slots 0/1 are reused for u, v
+  const size_t smem = (size_t)F::TR * F::RS * 8 + (size_t)slots * F::TR * F::S * 8;
+  auto kern = a.beta == 1   ? ks_row_kernel<P1, P2, 1>
+              : a.beta == 2 ? ks_row_kernel<P1, P2, 2>
+              : a.beta == 3 ? ks_row_kernel<P1, P2, 3>
+              : a.beta == 4 ? ks_row_kernel<P1, P2, 4>
+                            : ks_row_kernel<P1, P2, 0>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<dim3((1 << P1) / F::TR, rows, batch), F::NT, smem, st>>>(a);
+  return 0;
+}
+
+template <int P1, int P2>
+static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
+  using F = FusedCfg<P2>;
+  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, rows, batch), F::NT, 0, st>>>(a);
+  return 0;
+}
+
+bool fused_supported(int logn) { return logn >= 12 && logn <= 17; }
+
+int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
+  if (rows <= 0 || batch <= 0) return 0;
+  if (a.beta < 1 || a.beta > 8) return CK_ERR_ARG;
+  count_launches(1);
+  switch (a.logn) {
+    case 12: launch_ks_row_t<6, 6>(a, rows, batch, st); break;
+    case 13: launch_ks_row_t<6, 7>(a, rows, batch, st); break;
+    case 14: launch_ks_row_t<7, 7>(a, rows, batch, st); break;
+    case 15: launch_ks_row_t<7, 8>(a, rows, batch, st); break;
+    case 16: launch_ks_row_t<8, 8>(a, rows, batch, st); break;
+    case 17: launch_ks_row_t<8, 9>(a, rows, batch, st); break;
+    default: return CK_ERR_ARG;
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
+  if (rows <= 0 || batch <= 0) return 0;
+  count_launches(1);
+  switch (a.logn) {
+    case 12: launch_md_row_t<6, 6>(a, rows, batch, st); break;
+    case 13: launch_md_row_t<6, 7>(a, rows, batch, st); break;
+    case 14: launch_md_row_t<7, 7>(a, rows, batch, st); break;
+    case 15: launch_md_row_t<7, 8>(a, rows, batch, st); break;
+    case 16: launch_md_row_t<8, 8>(a, rows, batch, st); break;
+    case 17: launch_md_row_t<8, 9>(a, rows, batch, st); break;
+    default: return CK_ERR_ARG;
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace ck

@@ -31,14 +31,15 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
   for (int r = 0; r < kE; ++r) x[r] = base[((long long)sub_index<P1, 0, INV>(g, r) << P2) + c];
   __syncthreads();
-  run_pass<P1, 0, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+  run_pass<P1, 0, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
   if constexpr (NP > 1) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) sm[sub_index<P1, 0, INV>(g, r) * kTC + col] = x[r];
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 1, INV>(g, r) * kTC + col];
-    run_pass<P1, 1, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P1, 1, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
   }
   if constexpr (NP > 2) {
     __syncthreads();
@@ -47,7 +48,8 @@ ntt_col_kernel(NttArgs a) {
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 2, INV>(g, r) * kTC + col];
-    run_pass<P1, 2, INV, true>(x, g, c, P2, a.logn, tws, q, two_q);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P1, 2, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
   }
   static_assert(NP <= 3, "sub-transform too large");
   if (INV) {
@@ -57,7 +59,7 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = shoup(x[r], s.x, s.y, q);
   }
-  // forward: values stay lazy in [0,4q) for the row phase
+  // forward: values stay lazy in [0,16q) for the row phase
 #pragma unroll
   for (int r = 0; r < kE; ++r)
     base[((long long)sub_index<P1, NP - 1, INV>(g, r) << P2) + c] = x[r];
@@ -103,7 +105,8 @@ ntt_row_kernel(NttArgs a) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 0, INV>(g, r))];
   }
-  run_pass<P2, 0, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+  if (!INV) fwd_fold(x, q << 3);
+  run_pass<P2, 0, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
   if constexpr (NP > 1) {
     __syncthreads();
 #pragma unroll
@@ -111,7 +114,8 @@ ntt_row_kernel(NttArgs a) {
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 1, INV>(g, r))];
-    run_pass<P2, 1, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P2, 1, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
   }
   if constexpr (NP > 2) {
     __syncthreads();
@@ -120,14 +124,15 @@ ntt_row_kernel(NttArgs a) {
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 2, INV>(g, r))];
-    run_pass<P2, 2, INV, false>(x, g, jbase, 0, a.logn, tw, q, two_q);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P2, 2, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
   }
   static_assert(NP <= 3, "sub-transform too large");
   if (!INV) {
     // end of the forward transform: canonical residues; stores staged
     // through smem so the global writes are coalesced
 #pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = csub(csub(x[r], two_q), q);
+    for (int r = 0; r < kE; ++r) x[r] = fwd_final(x[r], q);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, NP - 1, INV>(g, r))] = x[r];
@@ -185,39 +190,48 @@ __global__ void __launch_bounds__(512) ntt_small_kernel(NttArgs a) {
 
 // ------------------------------------------------------------------ launch
 template <int P1, int P2>
-static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, cudaStream_t st) {
+static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int phase,
+                         cudaStream_t st) {
   const dim3 gcol((1 << P2) / kTC, jobs, batch), bcol(kTC * (1 << P1) / kE);
   using R = RowCfg<P2>;
   const dim3 grow((1 << P1) / R::TR, jobs, batch), brow(R::TR * R::G);
-  count_launches(2);
+  const bool col = phase != 2, row = phase != 1;
+  count_launches((int)col + (int)row);
   if (!inv) {
-    ntt_col_kernel<P1, P2, false><<<gcol, bcol, 0, st>>>(a);
-    ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
+    if (col) ntt_col_kernel<P1, P2, false><<<gcol, bcol, 0, st>>>(a);
+    if (row) ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
   } else {
-    ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
-    ntt_col_kernel<P1, P2, true><<<gcol, bcol, 0, st>>>(a);
+    if (row) ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
+    if (col) ntt_col_kernel<P1, P2, true><<<gcol, bcol, 0, st>>>(a);
   }
 }
 
-int launch_ntt(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st) {
+// phase: 0 = full transform, 1 = column phase only, 2 = row phase only
+// (split transforms are used by the fused key-switch; logn >= 12 only).
+int launch_ntt_phase(const NttArgs& a, int jobs, int batch, bool inverse, int phase,
+                     cudaStream_t st) {
   if (jobs <= 0 || batch <= 0) return 0;
   switch (a.logn) {
-    case 12: launch_split<6, 6>(a, jobs, batch, inverse, st); break;
-    case 13: launch_split<6, 7>(a, jobs, batch, inverse, st); break;
-    case 14: launch_split<7, 7>(a, jobs, batch, inverse, st); break;
-    case 15: launch_split<7, 8>(a, jobs, batch, inverse, st); break;
-    case 16: launch_split<8, 8>(a, jobs, batch, inverse, st); break;
-    case 17: launch_split<8, 9>(a, jobs, batch, inverse, st); break;
+    case 12: launch_split<6, 6>(a, jobs, batch, inverse, phase, st); break;
+    case 13: launch_split<6, 7>(a, jobs, batch, inverse, phase, st); break;
+    case 14: launch_split<7, 7>(a, jobs, batch, inverse, phase, st); break;
+    case 15: launch_split<7, 8>(a, jobs, batch, inverse, phase, st); break;
+    case 16: launch_split<8, 8>(a, jobs, batch, inverse, phase, st); break;
+    case 17: launch_split<8, 9>(a, jobs, batch, inverse, phase, st); break;
     default: {
-      if (a.logn < 1 || a.logn > 11) return CK_ERR_ARG;
-      const int n = 1 << a.logn;
+      if (phase != 0 || a.logn < 1 || a.logn > 11) return CK_ERR_ARG;
       count_launches(1);
+      const int n = 1 << a.logn;
       const dim3 grid(1, jobs, batch), blk(n / 2 < 512 ? (n / 2 > 0 ? n / 2 : 1) : 512);
       if (inverse) ntt_small_kernel<true><<<grid, blk, n * sizeof(u64), st>>>(a);
       else ntt_small_kernel<false><<<grid, blk, n * sizeof(u64), st>>>(a);
     }
   }
   return (int)cudaGetLastError();
+}
+
+int launch_ntt(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st) {
+  return launch_ntt_phase(a, jobs, batch, inverse, 0, st);
 }
 
 }  // namespace ck

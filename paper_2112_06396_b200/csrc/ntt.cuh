@@ -60,10 +60,14 @@ CK_D int sub_index(int g, int r) {
   return (blk << (LD + C)) + lo + (k << LD);
 }
 
-// One register pass.  j(s) = jbase + (s << jshift) is the limb-global index.
-template <int P, int p, bool INV, bool TW_SMEM>
-CK_D void run_pass(u64 (&x)[kE], int g, int jbase, int jshift, int logn,
-                   const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
+// One register pass.  j(s) = jbase + (s << JSHIFT) is the limb-global index.
+// Forward passes skip the per-butterfly correction: inputs in [0, 8q) grow
+// by 2q per stage to < 16q < 2^64 (q < 2^60); the caller folds them back
+// with one csub(8q) per element per pass (fwd_fold) -- half the ALU work of
+// Harvey's per-butterfly correction.
+template <int P, int p, bool INV, bool TW_SMEM, int LOGN, int JSHIFT>
+CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict__ tw, u64 q,
+                   u64 two_q) {
   constexpr int C = Sched<P>::C(p);
   constexpr int LD = Sched<P>::logD(p, INV);
   constexpr int NG = kE >> C;
@@ -75,23 +79,92 @@ CK_D void run_pass(u64 (&x)[kE], int g, int jbase, int jshift, int logn,
       // forward: distances shrink (half = 2^(C-1-st)); inverse: grow (2^st)
       const int lhalf = INV ? st : (C - 1 - st);
       const int half = 1 << lhalf;
-      const int logt = LD + lhalf + jshift;  // log2 of limb-global distance
-      const int logm = logn - 1 - logt;      // stage m (fwd) or h (inv)
+      const int logt = LD + lhalf + JSHIFT;  // log2 of limb-global distance
+      const int logm = LOGN - 1 - logt;      // stage m (fwd) or h (inv)
 #pragma unroll
       for (int b = 0; b < (1 << C) / (2 * half); ++b) {
         const int k0 = b * 2 * half;
-        const int j = jbase + ((s0 + (k0 << LD)) << jshift);
+        const int j = jbase + ((s0 + (k0 << LD)) << JSHIFT);
         const int idx = (1 << logm) + (j >> (logt + 1));
         ulonglong2 w;
         if (TW_SMEM) w = tw[idx];
         else w = __ldg(tw + idx);
 #pragma unroll
         for (int k = k0; k < k0 + half; ++k) {
-          if (INV) bfly_gs(x[(h << C) + k], x[(h << C) + k + half], w.x, w.y, q, two_q);
-          else bfly_ct(x[(h << C) + k], x[(h << C) + k + half], w.x, w.y, q, two_q);
+          u64& X = x[(h << C) + k];
+          u64& Y = x[(h << C) + k + half];
+          if (INV) {
+            bfly_gs(X, Y, w.x, w.y, q, two_q);
+          } else {
+            const u64 t = shoup_lazy(Y, w.x, w.y, q);
+            const u64 xx = X;
+            X = xx + t;
+            Y = xx - t + two_q;
+          }
         }
       }
     }
+  }
+}
+
+// Forward lazy range maintenance: [0, 16q) -> [0, 8q).
+CK_D void fwd_fold(u64 (&x)[kE], u64 q8) {
+#pragma unroll
+  for (int r = 0; r < kE; ++r) x[r] = csub(x[r], q8);
+}
+// [0, 16q) -> [0, q)
+CK_D u64 fwd_final(u64 v, u64 q) {
+  v = csub(v, q << 3);
+  v = csub(v, q << 2);
+  v = csub(v, q << 1);
+  return csub(v, q);
+}
+
+// ---------------------------------------------------------------- row helpers
+// A "row" is 2^P2 contiguous elements held by G = 2^P2/16 threads (thread g);
+// srow is that row's padded shared-memory slice (row_stride<P2>() entries).
+template <int P2>
+CK_HD constexpr int row_stride() { return (1 << P2) + (1 << P2) / 16; }
+CK_D int sidx(int s) { return s + (s >> 4); }
+
+template <int P2, int p, bool INV>
+CK_D void row_to_smem(const u64 (&x)[kE], int g, u64* srow) {
+#pragma unroll
+  for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, p, INV>(g, r))] = x[r];
+}
+template <int P2, int p, bool INV>
+CK_D void row_from_smem(u64 (&x)[kE], int g, const u64* srow) {
+#pragma unroll
+  for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, p, INV>(g, r))];
+}
+
+// Full row phase of a forward (INV=false) or inverse transform.  On entry x
+// holds the pass-0 layout, on exit the last-pass layout.  Contains
+// __syncthreads(): every thread of the CTA must call it.  Forward inputs may
+// be lazy in [0, 16q); forward outputs are lazy in [0, 16q) (fwd_final to
+// finish); inverse inputs/outputs are in [0, 2q).
+template <int P2, bool INV, int LOGN>
+CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
+                        const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
+  constexpr int NP = Sched<P2>::np;
+  static_assert(NP <= 3, "row too long");
+  if (!INV) fwd_fold(x, q << 3);
+  run_pass<P2, 0, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
+  if constexpr (NP > 1) {
+    __syncthreads();
+    row_to_smem<P2, 0, INV>(x, g, srow);
+    __syncthreads();
+    row_from_smem<P2, 1, INV>(x, g, srow);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P2, 1, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
+  }
+  if constexpr (NP > 2) {
+    __syncthreads();
+    row_to_smem<P2, 1, INV>(x, g, srow);
+    __syncthreads();
+    row_from_smem<P2, 2, INV>(x, g, srow);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass<P2, 2, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
   }
 }
 
