@@ -33,13 +33,17 @@ struct FusedCfg {
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
 // 2*BETA key loads of an element are independent and stay in flight);
 // BETA == 0: runtime a.beta (generic fallback).
+//
+// Shared memory: one padded row-tile slot per digit.  Slot d is digit d's
+// NTT exchange buffer and then holds its natural-order row, so the
+// automorphism gather happens at MAC time (one permutation index per element,
+// shared by all digits) -- no separate staging buffer.
 template <int P1, int P2, int BETA>
-__global__ void __launch_bounds__(FusedCfg<P2>::NT) ks_row_kernel(KsRowArgs a) {
+__global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
+  constexpr int SLOT = F::TR * F::RS;
   extern __shared__ __align__(16) u64 fsm[];
-  u64* stage = fsm;                     // [TR][RS] exchange / staging
-  u64* dsm = fsm + F::TR * F::RS;       // [beta][TR * S] gathered digits (MAC layout)
   const int i = blockIdx.y;
   const long long b = blockIdx.z;
   const int prime = a.prime[i];
@@ -47,20 +51,31 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) ks_row_kernel(KsRowArgs a) {
   const u64 q = P.q, two_q = P.two_q;
   const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
   const int r = blockIdx.x * F::TR + rl;
-  u64* srow = stage + rl * F::RS;
   const u64 t = a.galois ? a.galois[b] : a.galois_t;
   const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
   const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
+  constexpr int NB = BETA > 0 ? BETA : 8;
+  const int beta = BETA > 0 ? BETA : a.beta;
 
+  // Key tiles are only needed after the digit NTTs: start streaming them to L2
+  // now (one bulk prefetch per key row-tile, contiguous TR*S words), so the
+  // inner product below hits L2 instead of waiting on HBM.
+  if (threadIdx.x < 2 * beta) {
+    const int d = threadIdx.x >> 1;
+    const u64* kbase = (threadIdx.x & 1) ? a.key_a : a.key_b;
+    prefetch_l2(kbase + b * a.key_batch + d * a.key_digit_stride + ((long long)prime << LOGN) +
+                    ((long long)blockIdx.x * F::TR << P2),
+                F::TR * F::S * 8);
+  }
 #pragma unroll 1
-  for (int d = 0; d < a.beta; ++d) {
+  for (int d = 0; d < beta; ++d) {
     const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
+    u64* srow = fsm + d * SLOT + rl * F::RS;
     u64 x[kE];
     if (own) {
       const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
 #pragma unroll
       for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
-      __syncthreads();
       row_to_smem<P2, 0, false>(x, g, srow);
     } else {
       const u64* src = a.dig + b * a.dig_batch + ((long long)(d * a.R + i) << LOGN) +
@@ -73,69 +88,73 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) ks_row_kernel(KsRowArgs a) {
       __syncthreads();
       row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
     }
-    __syncthreads();
-    // gather: output column c of row r reads column pi_r(c) of row sigma(r)
-    u64* dd = dsm + (long long)d * (F::TR * F::S) + rl * F::S;
-#pragma unroll
-    for (int k = 0; k < kE; ++k) {
-      const int c = sub_index<P2, 0, false>(g, k);
-      const int sc = t == 1 ? c
-                            : (int)(automorph_src(((u32)r << P2) + c, (u32)t, LOGN) & (F::S - 1));
-      dd[c] = srow[sidx(sc)];
-    }
   }
+  __syncthreads();
 
-  // inner product with the key rows (coalesced: MAC layout = pass-0 layout)
-  const int krow = prime;
-  const u64* ka = a.key_a + b * a.key_batch + ((long long)krow << LOGN) + ((long long)r << P2);
-  const u64* kb = a.key_b + b * a.key_batch + ((long long)krow << LOGN) + ((long long)r << P2);
-  u64* uo = a.uv + b * a.uv_batch + ((long long)i << LOGN) + ((long long)r << P2);
+  // Inner product with the key rows.  MAC mapping (independent of the NTT
+  // layout): thread t owns element pairs e = 2t + 2*NT*m + {0,1} of the
+  // CTA's contiguous TR*S tile, so key loads / u,v stores are 16-byte
+  // vectors and every warp instruction covers 512 contiguous bytes.
+  // Output column c of row r reads column pi_r(c) of row sigma(r).
+  const long long tile0 = (long long)blockIdx.x * F::TR << P2;
+  const u64* ka = a.key_a + b * a.key_batch + ((long long)prime << LOGN) + tile0;
+  const u64* kb = a.key_b + b * a.key_batch + ((long long)prime << LOGN) + tile0;
+  u64* ubase = a.uv + b * a.uv_batch + ((long long)i << LOGN);
+  u64* uo = ubase + ((long long)r << P2);
   u64* vo = uo + a.v_off;
-  const bool inv_now = a.intt_special && i >= a.l;
-  u64* du = dsm + rl * F::S;                 // reused: u (digit slot 0), v (slot 1)
-  u64* dv = dsm + (F::TR * F::S) + rl * F::S;
-  constexpr int NB = BETA > 0 ? BETA : 8;
-  const int beta = BETA > 0 ? BETA : a.beta;
-#pragma unroll 4
-  for (int k = 0; k < kE; ++k) {
-    const int c = sub_index<P2, 0, false>(g, k);
-    Acc3 su, sv;
-    acc3_zero(su);
-    acc3_zero(sv);
+  constexpr int ITER = (F::TR * F::S) / (2 * F::NT);
+#pragma unroll 2
+  for (int m = 0; m < ITER; ++m) {
+    const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
+    const int er = e >> P2, ec = e & (F::S - 1);
+    const int rr = blockIdx.x * F::TR + er;
+    int sc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sc[h] = t == 1 ? ec + h
+                     : (int)(automorph_src(((u32)rr << P2) + ec + h, (u32)t, LOGN) & (F::S - 1));
+    Acc3 su[2], sv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      acc3_zero(su[h]);
+      acc3_zero(sv[h]);
+    }
 #pragma unroll
     for (int d = 0; d < NB; ++d) {
       if (BETA == 0 && d >= beta) break;
-      const u64 x = dsm[(long long)d * (F::TR * F::S) + rl * F::S + c];
-      const u64 ya = __ldg(ka + d * a.key_digit_stride + c);
-      const u64 yb = __ldg(kb + d * a.key_digit_stride + c);
-      const u32 x0 = lo30(x), x1 = hi30(x);
-      acc3_mac(su, x0, x1, lo30(ya), hi30(ya));
-      acc3_mac(sv, x0, x1, lo30(yb), hi30(yb));
+      const ulonglong2 ya = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + e));
+      const ulonglong2 yb = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + e));
+      const u64* drow = fsm + d * SLOT + er * F::RS;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const u64 x = drow[sidx(sc[h])];
+        const u64 ax = h ? ya.y : ya.x, bx = h ? yb.y : yb.x;
+        const u32 x0 = lo30(x), x1 = hi30(x);
+        acc3_mac(su[h], x0, x1, lo30(ax), hi30(ax));
+        acc3_mac(sv[h], x0, x1, lo30(bx), hi30(bx));
+      }
     }
-    const u64 uu = acc3_reduce(su, P), vv = acc3_reduce(sv, P);
-    if (inv_now) {
-      du[c] = uu;  // thread-private slots: every digit value at c is consumed
-      dv[c] = vv;
-    } else {
-      uo[c] = uu;
-      vo[c] = vv;
-    }
+    u64* uw = ubase + tile0 + e;
+    *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
+    *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
   }
-  if (inv_now) {
-    // first half of ModDown's INTT: inverse row phase, output lazy [0, 2q)
+  if (a.intt_special && i >= a.l) {
+    // first half of ModDown's INTT on the special rows: re-read the row this
+    // CTA just wrote (L1/L2 hit; __syncthreads orders the global accesses),
+    // inverse row phase, overwrite lazily in [0, 2q)
     const ulonglong2* itw = a.itw + ((long long)prime << LOGN);
+    u64* srow = fsm + rl * F::RS;
     u64 y[kE];
-    __syncthreads();
+#pragma unroll 1
+    for (int w = 0; w < 2; ++w) {
+      u64* io = w ? vo : uo;
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kE; ++k) y[k] = du[sub_index<P2, 0, true>(g, k)];
-    row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
+      for (int k = 0; k < kE; ++k) y[k] = io[sub_index<P2, 0, true>(g, k)];
+      row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
 #pragma unroll
-    for (int k = 0; k < kE; ++k) uo[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
-#pragma unroll
-    for (int k = 0; k < kE; ++k) y[k] = dv[sub_index<P2, 0, true>(g, k)];
-    row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
-#pragma unroll
-    for (int k = 0; k < kE; ++k) vo[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
+      for (int k = 0; k < kE; ++k) io[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
+    }
   }
 }
 
@@ -200,8 +219,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
 template <int P1, int P2>
 static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
-  const int slots = a.beta < 2 ? 2 : a.beta;  // >= 2: slots 0/1 are reused for u, v
-  const size_t smem = (size_t)F::TR * F::RS * 8 + (size_t)slots * F::TR * F::S * 8;
+  const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
   auto kern = a.beta == 1   ? ks_row_kernel<P1, P2, 1>
               : a.beta == 2 ? ks_row_kernel<P1, P2, 2>
               : a.beta == 3 ? ks_row_kernel<P1, P2, 3>

@@ -108,3 +108,9 @@ CK_D u32 automorph_src(u32 i, u32 t, int logn) {
   u32 e = (u32)(((u64)t * (2u * j + 1u)) & ((2ull << logn) - 1));
   return brev_bits((e - 1u) >> 1, logn);
 }
+
+// Bulk L2 prefetch (sm_90+): pull `bytes` (multiple of 16, 16-B aligned)
+// toward L2 without touching shared memory or registers.
+CK_D void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
