@@ -146,6 +146,9 @@ struct LevelTab {
 struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
+  int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
+  int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
+  int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = whole batch)
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   ulonglong2* d_tw = nullptr;
@@ -431,10 +434,10 @@ Ws ws_layout(const ck_plan* p, int l, int batch, u64* base) {
   const LevelTab& t = p->lv[l];
   const long long N = p->n, B = batch;
   Ws w;
-  w.tmp = base;
+  w.rot = base;  // conjugate's automorphed (a, b): whole batch
+  w.tmp = w.rot + B * 2 * l * N;
   w.conv = w.tmp + B * l * N;
-  w.rot = w.conv + B * 2 * l * N;
-  w.uv = w.rot + B * 2 * l * N;
+  w.uv = w.conv + B * 2 * l * N;
   w.dig = w.uv + B * 2 * t.R * N;
   return w;
 }
@@ -545,6 +548,8 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ka_.R = (int)R;
   ka_.logn = p->logn;
   ka_.intt_special = 1;
+  ka_.dbg = p->ks_dbg;
+  ka_.ws = p->ks_ws;
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
@@ -619,6 +624,12 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   {
     const char* e = getenv("CKB200_UNFUSED");
     p->fused = !(e && e[0] == '1');
+    const char* d = getenv("CKB200_KSDBG");
+    p->ks_dbg = d ? atoi(d) : 0;
+    const char* wsv = getenv("CKB200_KSWS");
+    p->ks_ws = wsv ? atoi(wsv) : 0;
+    const char* c = getenv("CKB200_CHUNK");
+    if (c) p->chunk = atoi(c);
   }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
@@ -845,9 +856,25 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
     egt = 1;
     kgal = nullptr;
   }
-  if (ck::fused_supported(p->logn) && p->fused)
-    return rotate_fused(p, level, a_src, b_add, key_b, key_a, kgt, kgal, egt,
-                        mode == 1 ? nullptr : galois, out_a, out_b, w, batch, st);
+  if (ck::fused_supported(p->logn) && p->fused) {
+    // L2-resident chunks: the pipeline runs on `chunk` key-switches at a time
+    // with the SAME workspace addresses, so every intermediate (INTT'd a,
+    // ModUp targets, u/v special rows, converted rows; ~80 MB per C3
+    // key-switch) is produced and consumed inside the 126 MB L2 -- the B200
+    // form of the paper's limb/accumulator caching.  Only inputs, keys and
+    // outputs stream from HBM.
+    const int C = p->chunk > 0 ? std::min(p->chunk, batch) : batch;
+    const long long kbatch = (long long)p->key_digits * (p->L + p->K) * N;
+    const u64* egal = mode == 1 ? nullptr : galois;
+    for (int c0 = 0; c0 < batch; c0 += C) {
+      const int cc = std::min(C, batch - c0);
+      CK_TRY(rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N, key_b + c0 * kbatch,
+                          key_a + c0 * kbatch, kgt, kgal ? kgal + c0 : nullptr, egt,
+                          egal ? egal + c0 : nullptr, out_a + c0 * l * N, out_b + c0 * l * N, w,
+                          cc, st));
+    }
+    return 0;
+  }
   CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
   // uv: [B][2][R][N]
   CK_TRY(kskip_impl(p, level, w.dig, key_b, key_a, kgt, kgal, w.uv, w.uv + R * N, 2 * R * N,

@@ -43,6 +43,8 @@ struct KsRowArgs {
   u64 galois_t;
   int lo[16], hi[16];           // digit spans (chain rows)
   int beta, l, R, logn, intt_special;
+  int dbg;                      // timing experiments only (CKB200_KSDBG); 0 in production
+  int ws;                       // warp-specialised persistent variant (CKB200_KSWS)
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
 

@@ -18,16 +18,19 @@
 #include "ck_internal.h"
 #include "ntt.cuh"
 
+#include <algorithm>
+
 namespace ck {
 
-template <int P2>
+template <int P2, int EPC = 2048>
 struct FusedCfg {
   static constexpr int S = 1 << P2;
   static constexpr int G = S / kE;         // threads per row
-  static constexpr int TR = 2048 / S;      // rows per CTA (2048 elements)
-  static constexpr int NT = TR * G;        // 128 threads
+  static constexpr int TR = EPC / S;       // rows per CTA (EPC elements)
+  static constexpr int NT = TR * G;        // EPC / 16 threads
   static constexpr int RS = row_stride<P2>();
 };
+constexpr int kKsEpc = 2048;  // ks_row: small CTAs -> 8 resident per SM (phase diversity)
 
 // ---------------------------------------------------------------- KSKIP row
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
@@ -39,13 +42,13 @@ struct FusedCfg {
 // automorphism gather happens at MAC time (one permutation index per element,
 // shared by all digits) -- no separate staging buffer.
 template <int P1, int P2, int BETA>
-__global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a) {
-  using F = FusedCfg<P2>;
+__global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsRowArgs a) {
+  using F = FusedCfg<P2, kKsEpc>;
   constexpr int LOGN = P1 + P2;
   constexpr int SLOT = F::TR * F::RS;
   extern __shared__ __align__(16) u64 fsm[];
-  const int i = blockIdx.y;
-  const long long b = blockIdx.z;
+  const int i = blockIdx.z;            // grid (row tile, batch, limb): see ks_row_ws_kernel
+  const long long b = blockIdx.y;
   const int prime = a.prime[i];
   const PrimeConst& P = a.pc[prime];
   const u64 q = P.q, two_q = P.two_q;
@@ -67,12 +70,50 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a
                     ((long long)blockIdx.x * F::TR << P2),
                 F::TR * F::S * 8);
   }
+  if constexpr (BETA > 0) {
+    // All digits' source rows are requested up front with async copies into
+    // their own slots (natural order), so the loads of digits 1.. overlap the
+    // NTT of digit 0.  Each thread copies exactly the elements it will read
+    // back first, so only cp.async.wait_group is needed before use.
+#pragma unroll
+    for (int d = 0; d < BETA; ++d) {
+      const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
+      const u64* src = (own ? a.a_eval + b * a.a_batch + ((long long)i << LOGN)
+                            : a.dig + b * a.dig_batch + ((long long)(d * a.R + i) << LOGN)) +
+                       ((long long)sr << P2);
+      u64* srow = fsm + d * SLOT + rl * F::RS;
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const int s0 = sub_index<P2, 0, false>(g, k);
+        cp_async8(srow + sidx(s0), src + s0);
+      }
+      cp_async_commit();
+    }
+#pragma unroll
+    for (int d = 0; d < BETA; ++d) {
+      const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
+      u64* srow = fsm + d * SLOT + rl * F::RS;
+      if (d == 0) cp_async_wait<BETA - 1>();
+      else if (d == 1) cp_async_wait<(BETA >= 2 ? BETA - 2 : 0)>();
+      else if (d == 2) cp_async_wait<(BETA >= 3 ? BETA - 3 : 0)>();
+      else cp_async_wait<0>();
+      if (!own) {  // own rows are already in place (natural order)
+        u64 x[kE];
+        row_from_smem<P2, 0, false>(x, g, srow);
+        row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
+#pragma unroll
+        for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+        __syncthreads();
+        row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+      }
+    }
+  } else {
 #pragma unroll 1
   for (int d = 0; d < beta; ++d) {
     const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
     u64* srow = fsm + d * SLOT + rl * F::RS;
     u64 x[kE];
-    if (own) {
+    if (own || (a.dbg & 1)) {
       const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
 #pragma unroll
       for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
@@ -89,6 +130,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a
       row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
     }
   }
+  }
   __syncthreads();
 
   // Inner product with the key rows.  MAC mapping (independent of the NTT
@@ -104,7 +146,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a
   u64* vo = uo + a.v_off;
   constexpr int ITER = (F::TR * F::S) / (2 * F::NT);
 #pragma unroll 2
-  for (int m = 0; m < ITER; ++m) {
+  for (int m = 0; m < ((a.dbg & 2) ? 0 : ITER); ++m) {
     const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
     const int er = e >> P2, ec = e & (F::S - 1);
     const int rr = blockIdx.x * F::TR + er;
@@ -138,7 +180,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a
     *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
     *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
   }
-  if (a.intt_special && i >= a.l) {
+  if (a.intt_special && i >= a.l && !(a.dbg & 4)) {
     // first half of ModDown's INTT on the special rows: re-read the row this
     // CTA just wrote (L1/L2 hit; __syncthreads orders the global accesses),
     // inverse row phase, overwrite lazily in [0, 2q)
@@ -158,14 +200,154 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 4) ks_row_kernel(KsRowArgs a
   }
 }
 
+// ------------------------------------------------- KSKIP row, warp-specialised
+// Persistent CTAs of two 128-thread warp groups and two SMEM buffers:
+//   group A (NTT):  digits of tile k -> buffer k%2 (loads, row NTT, staging)
+//   group B (MAC):  inner product of tile k-1 from buffer (k-1)%2 with key
+//                   rows streamed from HBM, + INTT row phase of special rows
+// handed over with named barriers (FULL/EMPTY per buffer), so the compute-
+// bound NTT of one tile overlaps the key-streaming MAC of the previous one.
+enum { kBarFull0 = 1, kBarEmpty0 = 3, kBarA = 5, kBarB = 6 };
+
+template <int P1, int P2, int BETA>
+__global__ void __launch_bounds__(2 * FusedCfg<P2, kKsEpc>::NT, 2)
+ks_row_ws_kernel(KsRowArgs a, int total_tiles) {
+  using F = FusedCfg<P2, kKsEpc>;
+  constexpr int LOGN = P1 + P2;
+  constexpr int SLOT = F::TR * F::RS;
+  constexpr int NT = F::NT;
+  constexpr int TPL = (1 << P1) / F::TR;  // row tiles per limb
+  extern __shared__ __align__(16) u64 fsm[];
+  const bool grpA = threadIdx.x < NT;
+  const int tid = grpA ? threadIdx.x : threadIdx.x - NT;
+  const int rl = tid / F::G, g = tid % F::G;
+  int k = 0;
+  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++k) {
+    const int sbuf = k & 1;
+    u64* buf = fsm + sbuf * (BETA * SLOT);
+    // row tile fastest, then batch item, then limb: consecutive tiles share
+    // the limb's prime, so its row twiddles stay in L1/L2 across the batch
+    const int rt = tile % TPL;
+    const int nb = total_tiles / (TPL * a.R);
+    const long long b = (tile / TPL) % nb;
+    const int i = tile / (TPL * nb);
+    const int prime = a.prime[i];
+    const PrimeConst& P = a.pc[prime];
+    const u64 q = P.q, two_q = P.two_q;
+    const u64 t = a.galois ? a.galois[b] : a.galois_t;
+    if (grpA) {
+      // ---------------- producer: digit rows -> NTT row phase -> natural order
+      if (k >= 2) bar_sync_n(kBarEmpty0 + sbuf, 2 * NT);
+      const int r = rt * F::TR + rl;
+      const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
+      const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
+      if (tid < 2 * BETA) {  // keys of this tile toward L2 for group B
+        const int d = tid >> 1;
+        const u64* kbase = (tid & 1) ? a.key_a : a.key_b;
+        prefetch_l2(kbase + b * a.key_batch + d * a.key_digit_stride + ((long long)prime << LOGN) +
+                        ((long long)rt * F::TR << P2),
+                    F::TR * F::S * 8);
+      }
+#pragma unroll 1
+      for (int d = 0; d < BETA; ++d) {
+        const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
+        u64* srow = buf + d * SLOT + rl * F::RS;
+        u64 x[kE];
+        if (own) {
+          const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
+#pragma unroll
+          for (int kk = 0; kk < kE; ++kk) x[kk] = src[sub_index<P2, 0, false>(g, kk)];
+          row_to_smem<P2, 0, false>(x, g, srow);
+        } else {
+          const u64* src = a.dig + b * a.dig_batch + ((long long)(d * a.R + i) << LOGN) +
+                           ((long long)sr << P2);
+#pragma unroll
+          for (int kk = 0; kk < kE; ++kk) x[kk] = src[sub_index<P2, 0, false>(g, kk)];
+          row_transform<P2, false, LOGN, SyncGroup<kBarA, NT>>(x, g, sr << P2, srow, tw, q, two_q);
+#pragma unroll
+          for (int kk = 0; kk < kE; ++kk) x[kk] = fwd_final(x[kk], q);
+          bar_sync_n(kBarA, NT);
+          row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+        }
+      }
+      bar_arrive_n(kBarFull0 + sbuf, 2 * NT);
+    } else {
+      // ---------------- consumer: inner product with streamed key rows
+      bar_sync_n(kBarFull0 + sbuf, 2 * NT);
+      const long long tile0 = (long long)rt * F::TR << P2;
+      const u64* ka = a.key_a + b * a.key_batch + ((long long)prime << LOGN) + tile0;
+      const u64* kb = a.key_b + b * a.key_batch + ((long long)prime << LOGN) + tile0;
+      u64* ubase = a.uv + b * a.uv_batch + ((long long)i << LOGN);
+      constexpr int ITER = (F::TR * F::S) / (2 * NT);
+#pragma unroll 2
+      for (int m = 0; m < ITER; ++m) {
+        const int e = 2 * tid + 2 * NT * m;
+        const int er = e >> P2, ec = e & (F::S - 1);
+        const int rr = rt * F::TR + er;
+        int sc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          sc[h] = t == 1 ? ec + h
+                         : (int)(automorph_src(((u32)rr << P2) + ec + h, (u32)t, LOGN) & (F::S - 1));
+        Acc3 su[2], sv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          acc3_zero(su[h]);
+          acc3_zero(sv[h]);
+        }
+#pragma unroll
+        for (int d = 0; d < BETA; ++d) {
+          const ulonglong2 ya = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + e));
+          const ulonglong2 yb = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + e));
+          const u64* drow = buf + d * SLOT + er * F::RS;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const u64 x = drow[sidx(sc[h])];
+            const u64 ax = h ? ya.y : ya.x, bx = h ? yb.y : yb.x;
+            const u32 x0 = lo30(x), x1 = hi30(x);
+            acc3_mac(su[h], x0, x1, lo30(ax), hi30(ax));
+            acc3_mac(sv[h], x0, x1, lo30(bx), hi30(bx));
+          }
+        }
+        u64* uw = ubase + tile0 + e;
+        *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
+        *(ulonglong2*)(uw + a.v_off) =
+            make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+      }
+      if (a.intt_special && i >= a.l) {
+        const int r = rt * F::TR + rl;
+        const ulonglong2* itw = a.itw + ((long long)prime << LOGN);
+        u64* srow = buf + rl * F::RS;  // buffer slot 0 as exchange space
+        u64* uo = ubase + ((long long)r << P2);
+        u64 y[kE];
+#pragma unroll 1
+        for (int w = 0; w < 2; ++w) {
+          u64* io = w ? uo + a.v_off : uo;
+          bar_sync_n(kBarB, NT);
+#pragma unroll
+          for (int kk = 0; kk < kE; ++kk) y[kk] = io[sub_index<P2, 0, true>(g, kk)];
+          row_transform<P2, true, LOGN, SyncGroup<kBarB, NT>>(y, g, r << P2, srow, itw, q, two_q);
+#pragma unroll
+          for (int kk = 0; kk < kE; ++kk) io[sub_index<P2, Sched<P2>::np - 1, true>(g, kk)] = y[kk];
+        }
+      }
+      bar_arrive_n(kBarEmpty0 + sbuf, 2 * NT);
+    }
+  }
+  // drain: the producer consumes the consumer's last EMPTY arrival per buffer
+  if (grpA) {
+    for (int s2 = 0; s2 < 2 && s2 < k; ++s2) bar_sync_n(kBarEmpty0 + ((k - 1 - s2) & 1), 2 * NT);
+  }
+}
+
 // ------------------------------------------------------------ ModDown row
 template <int P1, int P2>
 __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
   __shared__ u64 stage[F::TR * F::RS];
-  const int j = blockIdx.y;
-  const long long b = blockIdx.z;
+  const int j = blockIdx.z;  // grid (row tile, batch, limb): twiddle reuse across the batch
+  const long long b = blockIdx.y;
   const int prime = a.prime[j];
   const PrimeConst& P = a.pc[prime];
   const u64 q = P.q, two_q = P.two_q;
@@ -216,9 +398,32 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
 }
 
 // ------------------------------------------------------------------ launch
+template <int P1, int P2, int BETA>
+static void launch_ks_ws(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
+  using F = FusedCfg<P2, kKsEpc>;
+  const size_t smem = (size_t)2 * BETA * F::TR * F::RS * 8;
+  auto kern = ks_row_ws_kernel<P1, P2, BETA>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * F::NT, smem);
+  const int total = ((1 << P1) / F::TR) * rows * batch;
+  const int grid = std::min(total, sms * std::max(per_sm, 1));
+  kern<<<grid, 2 * F::NT, smem, st>>>(a, total);
+}
+
 template <int P1, int P2>
 static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
-  using F = FusedCfg<P2>;
+  using F = FusedCfg<P2, kKsEpc>;
+  if (a.ws && !a.dbg && a.beta >= 1 && a.beta <= 4) {
+    switch (a.beta) {
+      case 1: launch_ks_ws<P1, P2, 1>(a, rows, batch, st); return 0;
+      case 2: launch_ks_ws<P1, P2, 2>(a, rows, batch, st); return 0;
+      case 3: launch_ks_ws<P1, P2, 3>(a, rows, batch, st); return 0;
+      default: launch_ks_ws<P1, P2, 4>(a, rows, batch, st); return 0;
+    }
+  }
   const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
   auto kern = a.beta == 1   ? ks_row_kernel<P1, P2, 1>
               : a.beta == 2 ? ks_row_kernel<P1, P2, 2>
@@ -227,14 +432,14 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
                             : ks_row_kernel<P1, P2, 0>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<dim3((1 << P1) / F::TR, rows, batch), F::NT, smem, st>>>(a);
+  kern<<<dim3((1 << P1) / F::TR, batch, rows), F::NT, smem, st>>>(a);
   return 0;
 }
 
 template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
-  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, rows, batch), F::NT, 0, st>>>(a);
+  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, batch, rows), F::NT, 0, st>>>(a);
   return 0;
 }
 

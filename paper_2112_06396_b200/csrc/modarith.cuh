@@ -74,13 +74,16 @@ CK_D void acc3_mac(Acc3& s, u32 a0, u32 a1, u32 b0, u32 b1) {
 CK_D u32 lo30(u64 x) { return (u32)x & 0x3fffffffu; }
 CK_D u32 hi30(u64 x) { return (u32)(x >> 30); }
 
-// Reduce lo + mid*2^30 + hi*2^60 into [0, q).
+// Reduce lo + mid*2^30 + hi*2^60 into [0, q): assemble the exact 128-bit
+// value with funnel shifts and carries (ALU pipe), then one 128-bit
+// reduction (2 Shoup-style steps on the IMAD pipe instead of 3).
 CK_D u64 acc3_reduce(const Acc3& s, const PrimeConst& P) {
-  u64 r = red64_lazy(s.lo, P) + shoup_lazy(s.mid, P.c30, P.c30p, P.q) +
-          shoup_lazy(s.hi, P.c60, P.c60p, P.q);  // < 6q
-  r = csub(r, P.two_q << 1);
-  r = csub(r, P.two_q);
-  return csub(r, P.q);
+  u64 lo = s.lo, hi = 0;
+  const u64 m_lo = s.mid << 30, m_hi = s.mid >> 34;
+  const u64 h_lo = s.hi << 60, h_hi = s.hi >> 4;
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(m_lo), "l"(m_hi));
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(h_lo), "l"(h_hi));
+  return red128(hi, lo, P);
 }
 
 // ---- NTT butterflies (Harvey lazy) ----
@@ -114,3 +117,12 @@ CK_D u32 automorph_src(u32 i, u32 t, int logn) {
 CK_D void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+
+// Ampere-style async copies (LDGSTS): 8-byte global -> shared, grouped.
+CK_D void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+CK_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+CK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }

@@ -4,9 +4,8 @@
 
 namespace ck {
 
-CK_D long long job_offset(const NttArgs& a, int job) {
-  return (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) +
-         (long long)blockIdx.z * a.batch_stride;
+CK_D long long job_offset(const NttArgs& a, int job, int bz) {
+  return (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) + (long long)bz * a.batch_stride;
 }
 
 // ------------------------------------------------------------ column phase
@@ -24,7 +23,7 @@ ntt_col_kernel(NttArgs a) {
   const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
   const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
   for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
-  u64* base = a.data + job_offset(a, job);
+  u64* base = a.data + job_offset(a, job, blockIdx.z);
   const int col = threadIdx.x % kTC, g = threadIdx.x / kTC;
   const int c = blockIdx.x * kTC + col;
   u64 x[kE];
@@ -81,11 +80,11 @@ ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;
   __shared__ u64 sm[R::TR * R::RS];
-  const int job = blockIdx.y;
+  const int job = blockIdx.z;  // grid (row tile, batch, job): twiddle reuse across the batch
   const int prime = a.prime_idx[job];
   const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
   const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
-  u64* base = a.data + job_offset(a, job);
+  u64* base = a.data + job_offset(a, job, blockIdx.y);
   const int rl = threadIdx.x / R::G, g = threadIdx.x % R::G;
   const int row = blockIdx.x * R::TR + rl;
   u64* rowp = base + ((long long)row << P2);
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(512) ntt_small_kernel(NttArgs a) {
   const int prime = a.prime_idx[job];
   const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
   const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
-  u64* base = a.data + job_offset(a, job);
+  u64* base = a.data + job_offset(a, job, blockIdx.z);
   for (int i = threadIdx.x; i < n; i += blockDim.x) sx[i] = base[i];
   __syncthreads();
   if (!INV) {
@@ -194,7 +193,7 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
                          cudaStream_t st) {
   const dim3 gcol((1 << P2) / kTC, jobs, batch), bcol(kTC * (1 << P1) / kE);
   using R = RowCfg<P2>;
-  const dim3 grow((1 << P1) / R::TR, jobs, batch), brow(R::TR * R::G);
+  const dim3 grow((1 << P1) / R::TR, batch, jobs), brow(R::TR * R::G);
   const bool col = phase != 2, row = phase != 1;
   count_launches((int)col + (int)row);
   if (!inv) {

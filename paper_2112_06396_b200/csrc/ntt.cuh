@@ -143,7 +143,21 @@ CK_D void row_from_smem(u64 (&x)[kE], int g, const u64* srow) {
 // __syncthreads(): every thread of the CTA must call it.  Forward inputs may
 // be lazy in [0, 16q); forward outputs are lazy in [0, 16q) (fwd_final to
 // finish); inverse inputs/outputs are in [0, 2q).
-template <int P2, bool INV, int LOGN>
+// Barrier policies for row_transform: the whole CTA, or one warp group
+// (named barrier ID over NT threads) in warp-specialised kernels.
+struct SyncCta {
+  CK_D static void sync() { __syncthreads(); }
+};
+template <int ID, int NT>
+struct SyncGroup {
+  CK_D static void sync() { asm volatile("bar.sync %0, %1;" ::"r"(ID), "r"(NT) : "memory"); }
+};
+CK_D void bar_sync_n(int id, int nt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory"); }
+CK_D void bar_arrive_n(int id, int nt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nt) : "memory");
+}
+
+template <int P2, bool INV, int LOGN, class Sync = SyncCta>
 CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
                         const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
   constexpr int NP = Sched<P2>::np;
@@ -151,17 +165,17 @@ CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
   if (!INV) fwd_fold(x, q << 3);
   run_pass<P2, 0, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
   if constexpr (NP > 1) {
-    __syncthreads();
+    Sync::sync();
     row_to_smem<P2, 0, INV>(x, g, srow);
-    __syncthreads();
+    Sync::sync();
     row_from_smem<P2, 1, INV>(x, g, srow);
     if (!INV) fwd_fold(x, q << 3);
     run_pass<P2, 1, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
   }
   if constexpr (NP > 2) {
-    __syncthreads();
+    Sync::sync();
     row_to_smem<P2, 1, INV>(x, g, srow);
-    __syncthreads();
+    Sync::sync();
     row_from_smem<P2, 2, INV>(x, g, srow);
     if (!INV) fwd_fold(x, q << 3);
     run_pass<P2, 2, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
