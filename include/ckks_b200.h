@@ -120,6 +120,21 @@ int ck_rotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const u
               int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
               ck_stream stream);
 
+/* ---- hoisted BSGS linear transform (composites.py:249-293) ----
+ * == sum_{j=1..giant} rotate(pt_matvec(ct, {k: diag[j][k]}), -baby*j)  (ckks.py:684-719)
+ * One shared ModUp; `baby` KSKIPs (Galois 5^k, k = 1..baby) in one launch;
+ * diagonal MACs into `giant` raised accumulators; merged ModDown (P*q_last);
+ * `giant` batched rotations at level-1 (Galois 5^(baby*j)); sum.
+ * a, b: [level][N]; baby keys [baby][dnum][L+K][N]; giant keys [giant][...];
+ * diags: [giant][baby][level+K][N] raised-basis eval rows; galois arrays DEVICE.
+ * Output: [level-1][N] x 2.                                                  */
+size_t ck_bsgs_workspace_bytes(const ck_plan* plan, int level, int baby, int giant);
+int ck_bsgs(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* baby_key_b,
+            const uint64_t* baby_key_a, const uint64_t* giant_key_b, const uint64_t* giant_key_a,
+            const uint64_t* diags, const uint64_t* baby_galois, const uint64_t* giant_galois,
+            int level, int baby, int giant, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace,
+            ck_stream stream);
+
 /* ---- synthetic inputs: counter-based uniform residues (paper_2112_06396_b200.synth) ----
  * row r: out[r][k] = mulhi(splitmix64(keys[r] + k), qs[r]).  keys, qs: DEVICE. */
 int ck_fill_uniform(uint64_t* out, int64_t rows, int log_n, const uint64_t* keys,

@@ -39,6 +39,9 @@ _SIGS = [
     ("ck_moddown", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_uint64, vp, C.c_int, vp]),
     ("ck_rotate", C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_uint64, vp, C.c_int, vp, vp, vp,
                             C.c_int, vp]),
+    ("ck_bsgs_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int, C.c_int]),
+    ("ck_bsgs", C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp,
+                          vp, vp]),
     ("ck_fill_uniform", C.c_int, [vp, C.c_int64, C.c_int, vp, vp, vp]),
 ]
 

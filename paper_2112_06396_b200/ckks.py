@@ -367,32 +367,50 @@ def bsgs(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict, diag_del
          baby: int, giant: int) -> Ciphertext:
     """Hoisted BSGS linear transform (composites.py:249-293).
 
-    One shared ModUp; baby KSKIPs (k = 1..baby) reused by every giant group;
-    per group j the raised accumulators sum diags[(j, k)] * (u_k, v_k + P b_k),
-    one merged ModDown, then a full rotate by -baby*j at l-1; results summed.
+    One shared ModUp; baby KSKIPs (k = 1..baby, one launch) reused by every
+    giant group; per group j the raised accumulators sum
+    diags[(j, k)] * (u_k, v_k + P b_k), one merged ModDown, then a full rotate
+    by -baby*j at l-1 (batched); results summed -- all in ck_bsgs.
     Bit-identical to sum_j rotate(pt_matvec(ct, {k: diags[j,k]}), -baby*j).
     """
+    n = params.n_ring
     limbs = ct.limbs
     raised = params.raised_moduli(limbs)
-    dig = _decomp_modup_raw(params, ct.a.data, limbs)
-    baby_uv = {}
-    for k in range(1, baby + 1):
-        t = _galois(params, -k)
-        u, v = _kskip_raw(params, dig, keys.rot[-k], limbs, t)
-        vb = RnsPoly(raised, v, "eval").add(pmodup(params, ct.b.automorph(t)))
-        baby_uv[k] = (RnsPoly(raised, u, "eval"), vb)
-    out = None
-    for j in range(1, giant + 1):
-        acc_u = RnsPoly.zeros(raised, params.n_ring, "eval")
-        acc_v = RnsPoly.zeros(raised, params.n_ring, "eval")
-        for k in range(1, baby + 1):
-            m_hat = diags[(j, k)]
-            acc_u = acc_u.add(m_hat.mul(baby_uv[k][0]))
-            acc_v = acc_v.add(m_hat.mul(baby_uv[k][1]))
-        g = Ciphertext(_moddown_merged(params, acc_u, limbs), _moddown_merged(params, acc_v, limbs),
-                       ct.delta * diag_delta / raised[limbs - 1])
-        rj = rotate(params, keys, g, -baby * j)
-        out = rj if out is None else add(out, rj)
+    bkeys = [keys.rot[-k] for k in range(1, baby + 1)]
+    gkeys = [keys.rot[-baby * j] for j in range(1, giant + 1)]
+    bkb = torch.stack([k.b for k in bkeys]).contiguous()
+    bka = torch.stack([k.a for k in bkeys]).contiguous()
+    gkb = torch.stack([k.b for k in gkeys]).contiguous()
+    gka = torch.stack([k.a for k in gkeys]).contiguous()
+    for jk, d in diags.items():
+        assert d.moduli == raised, jk
+    dg = torch.stack([torch.stack([diags[(j, k)].data for k in range(1, baby + 1)])
+                      for j in range(1, giant + 1)]).contiguous()
+    out_a, out_b = bsgs_raw(params, ct.a.data, ct.b.data, bkb, bka, gkb, gka, dg, baby, giant)
+    mods = params.chain[:limbs - 1]
+    return Ciphertext(RnsPoly(mods, out_a, "eval"), RnsPoly(mods, out_b, "eval"),
+                      ct.delta * diag_delta / raised[limbs - 1])
+
+
+def bsgs_raw(params, a, b, bkb, bka, gkb, gka, diags, baby: int, giant: int, out=None, ws=None):
+    """ck_bsgs on pre-stacked device tensors (the benchmark's C4 unit)."""
+    plan = plan_for(params)
+    n = params.n_ring
+    limbs = a.shape[0]
+    bgal = torch.tensor(np.array([pow(5, k, 2 * n) for k in range(1, baby + 1)], dtype=np.uint64),
+                        device="cuda")
+    ggal = torch.tensor(np.array([pow(5, baby * j, 2 * n) for j in range(1, giant + 1)],
+                                 dtype=np.uint64), device="cuda")
+    if out is None:
+        out = (torch.empty((limbs - 1, n), dtype=torch.uint64, device="cuda"),
+               torch.empty((limbs - 1, n), dtype=torch.uint64, device="cuda"))
+    if ws is None:
+        nbytes = _L().ck_bsgs_workspace_bytes(plan.h, limbs, baby, giant)
+        assert nbytes > 0
+        ws = torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
+    check(_L().ck_bsgs(plan.h, ptr(a), ptr(b), ptr(bkb), ptr(bka), ptr(gkb), ptr(gka), ptr(diags),
+                       ptr(bgal), ptr(ggal), limbs, baby, giant, ptr(out[0]), ptr(out[1]), ptr(ws),
+                       stream_handle()), "ck_bsgs")
     return out
 
 

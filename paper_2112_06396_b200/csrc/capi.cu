@@ -467,13 +467,13 @@ int modup_impl(const ck_plan* p, int l, const u64* a, u64* digits, u64* tmp, int
 
 int kskip_impl(const ck_plan* p, int l, const u64* digits, const u64* kb, const u64* ka,
                u64 gt, const u64* galois, u64* u, u64* v, long long uv_batch, int B,
-               cudaStream_t st) {
+               cudaStream_t st, bool shared_digits = false) {
   const LevelTab& t = p->lv[l];
   const long long N = p->n;
   ck::KskipArgs a;
   a.digits = digits;
   a.digit_stride = (long long)t.R * N;
-  a.digits_batch = (long long)t.beta * t.R * N;
+  a.digits_batch = shared_digits ? 0 : (long long)t.beta * t.R * N;
   a.key_b = kb;
   a.key_a = ka;
   a.key_digit_stride = (long long)(p->L + p->K) * N;
@@ -857,12 +857,11 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
     kgal = nullptr;
   }
   if (ck::fused_supported(p->logn) && p->fused) {
-    // L2-resident chunks: the pipeline runs on `chunk` key-switches at a time
-    // with the SAME workspace addresses, so every intermediate (INTT'd a,
-    // ModUp targets, u/v special rows, converted rows; ~80 MB per C3
-    // key-switch) is produced and consumed inside the 126 MB L2 -- the B200
-    // form of the paper's limb/accumulator caching.  Only inputs, keys and
-    // outputs stream from HBM.
+    // Optional chunking (CKB200_CHUNK): run the pipeline on `chunk`
+    // key-switches at a time with the same workspace addresses so the
+    // intermediates stay L2-resident.  Measured slower than one pass over the
+    // whole batch (the kernels are INT-bound and want the parallelism), so the
+    // default is 0 = whole batch; see DESIGN.md section 5.
     const int C = p->chunk > 0 ? std::min(p->chunk, batch) : batch;
     const long long kbatch = (long long)p->key_digits * (p->L + p->K) * N;
     const u64* egal = mode == 1 ? nullptr : galois;
@@ -887,6 +886,95 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
   return ew_run(p, ck::EW_MODDOWN, out_b, l * N, w.uv + R * N, 2 * R * N, w.conv + l * N,
                 2 * l * N, b_add, l * N, m.d_keep_prime, m.d_pinv, egt, mode == 1 ? nullptr : galois,
                 level, batch, st);
+}
+
+size_t ck_bsgs_workspace_bytes(const ck_plan* p, int level, int baby, int giant) {
+  if (!level_ok(p, level) || level < 2 || baby < 1 || giant < 1) return 0;
+  const LevelTab& t = p->lv[level];
+  const long long N = p->n, l = level, R = t.R;
+  const long long rows = (long long)t.beta * R + l + (long long)baby * 2 * R +
+                         (long long)giant * 2 * R + (long long)giant * 2 * l +
+                         (long long)giant * 4 * (l - 1);
+  return (size_t)rows * N * sizeof(u64) + ck_workspace_bytes(p, level - 1, giant);
+}
+
+int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* bkb_,
+            const uint64_t* bka_, const uint64_t* gkb_, const uint64_t* gka_,
+            const uint64_t* diags_, const uint64_t* baby_galois_, const uint64_t* giant_galois_,
+            int level, int baby, int giant, uint64_t* out_a_, uint64_t* out_b_,
+            uint64_t* workspace_, ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *bkb = (const u64*)bkb_,
+            *bka = (const u64*)bka_, *gkb = (const u64*)gkb_, *gka = (const u64*)gka_,
+            *diags = (const u64*)diags_, *bgal = (const u64*)baby_galois_,
+            *ggal = (const u64*)giant_galois_;
+  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
+  if (!level_ok(p, level) || level < 2 || !a || !b || !bkb || !bka || !gkb || !gka || !diags ||
+      !bgal || !ggal || !out_a || !out_b || !ws || baby < 1 || baby > 32 || giant < 1 ||
+      p->K < 1)
+    return CK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const LevelTab& t = p->lv[level];
+  const ModDownTab& m = t.md[1];
+  const long long N = p->n, l = level, R = t.R, lo = l - 1;
+  u64* dig = ws;
+  u64* tmp = dig + (long long)t.beta * R * N;
+  u64* uvb = tmp + l * N;                       // [baby][2][R][N]
+  u64* acc = uvb + (long long)baby * 2 * R * N; // [giant][2][R][N]
+  u64* conv = acc + (long long)giant * 2 * R * N;
+  u64* ga = conv + (long long)giant * 2 * l * N; // [giant][l-1][N]
+  u64* gb = ga + (long long)giant * lo * N;
+  u64* ra = gb + (long long)giant * lo * N;      // rotated giants
+  u64* rb = ra + (long long)giant * lo * N;
+  u64* rws = rb + (long long)giant * lo * N;
+  // 1. one shared ModUp (hoisting)
+  CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
+  // 2. all baby KSKIPs in one launch: digits shared, per-baby key and Galois element
+  CK_TRY(kskip_impl(p, level, dig, bkb, bka, 1, bgal, uvb, uvb + R * N, 2 * R * N, baby, st,
+                    true));
+  // 3. diagonal MAC into giant accumulators (pmodup(automorph(b)) folded in)
+  ck::DiagArgs da;
+  da.uv = uvb;
+  da.b = b;
+  da.diags = diags;
+  da.acc = acc;
+  da.galois = bgal;
+  da.prime = t.d_raised_prime;
+  da.pmod = t.d_pmod;
+  da.pc = p->d_pc;
+  da.baby = baby;
+  da.giant = giant;
+  da.R = (int)R;
+  da.l = level;
+  da.logn = p->logn;
+  CK_TRY(ck::launch_diag_mac(da, st));
+  // 4. merged ModDown (P * q_last) of every accumulator -> level l-1
+  CK_TRY(moddown_core(p, m, acc, R * N, conv, 2 * giant, st));
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, ga, lo * N, acc, 2 * R * N, conv, 2 * lo * N, nullptr, 0,
+                m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, gb, lo * N, acc + R * N, 2 * R * N, conv + lo * N, 2 * lo * N,
+                nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
+  // 5. giant rotations at l-1, batched
+  CK_TRY(ck_rotate(p, (const uint64_t*)ga, (const uint64_t*)gb, gkb_, gka_, (int)lo, 1,
+                   giant_galois_, 0, (uint64_t*)ra, (uint64_t*)rb, (uint64_t*)rws, giant, stream));
+  // 6. sum of the rotated giants
+  const int* kp = p->lv[lo].d_chain_prime;
+  if (giant == 1) {
+    CK_TRY(ew_run(p, ck::EW_COPY, out_a, 0, ra, 0, nullptr, 0, nullptr, 0, kp, nullptr, 1, nullptr,
+                  (int)lo, 1, st));
+    return ew_run(p, ck::EW_COPY, out_b, 0, rb, 0, nullptr, 0, nullptr, 0, kp, nullptr, 1, nullptr,
+                  (int)lo, 1, st);
+  }
+  CK_TRY(ew_run(p, ck::EW_ADD, out_a, 0, ra, 0, ra + lo * N, 0, nullptr, 0, kp, nullptr, 1,
+                nullptr, (int)lo, 1, st));
+  CK_TRY(ew_run(p, ck::EW_ADD, out_b, 0, rb, 0, rb + lo * N, 0, nullptr, 0, kp, nullptr, 1,
+                nullptr, (int)lo, 1, st));
+  for (int j = 2; j < giant; ++j) {
+    CK_TRY(ew_run(p, ck::EW_ADD, out_a, 0, out_a, 0, ra + j * lo * N, 0, nullptr, 0, kp, nullptr,
+                  1, nullptr, (int)lo, 1, st));
+    CK_TRY(ew_run(p, ck::EW_ADD, out_b, 0, out_b, 0, rb + j * lo * N, 0, nullptr, 0, kp, nullptr,
+                  1, nullptr, (int)lo, 1, st));
+  }
+  return 0;
 }
 
 int ck_fill_uniform(uint64_t* out_, int64_t rows, int log_n, const uint64_t* keys_,

@@ -67,6 +67,20 @@ struct MdRowArgs {
 };
 int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st);
 
+// BSGS diagonal multiply-accumulate (bsgs.cu)
+struct DiagArgs {
+  const u64* uv;                // [baby][2][R][N]
+  const u64* b;                 // [l][N]
+  const u64* diags;             // [giant][baby][R][N]
+  u64* acc;                     // [giant][2][R][N]
+  const u64* galois;            // [baby] device
+  const int* prime;             // [R]
+  const ulonglong2* pmod;       // [l] [P]_q Shoup pairs
+  const PrimeConst* pc;
+  int baby, giant, R, l, logn;
+};
+int launch_diag_mac(const DiagArgs& a, cudaStream_t st);
+
 // Basis conversion: ns source rows (coefficient rep, same coefficient index)
 // -> nd destination rows.  T[i*nd+j] = (Q/q_i) mod p_j.
 struct BconvArgs {
