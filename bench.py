@@ -305,13 +305,82 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
+def run_config(args, rank: int, world: int, local_rank: int):
+    """Non-default BASELINE configs (C1, C2, C4, C5): device-resident throughput only."""
+    import torch
+    import torch.distributed as dist
+    from paper_2112_06396_b200 import _lib
+    from paper_2112_06396_b200.params import config, galois_exponents
+    from paper_2112_06396_b200 import workload as W
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lib = _lib.load()
+    wl = config(args.config)
+    p = wl.params
+    if wl.kind == "rotate":
+        B = args.batch if args.batch_set else {"C1": 1, "C5": 32}.get(args.config, 64)
+        units = [rank * B + i for i in range(B)]
+        allk = galois_exponents(p.n_ring, B * world, SEED)
+        job = W.RotationBatch(p, SEED, units, ks=[allk[u] for u in units])
+        per_step, unit, bytes_unit = B, "key-switches/s", ks_bytes(p)
+    elif wl.kind == "ntt":
+        job = W.NttBatch(p, SEED, 16)
+        per_step, unit = 16 * p.limbs, "limb NTT+INTT round trips/s"
+        bytes_unit = 4 * 8 * p.n_ring
+    else:
+        job = W.BsgsWorkload(p, SEED)
+        per_step, unit, bytes_unit = 1, "BSGS transforms/s", job.algorithmic_bytes()
+    for _ in range(args.warmup):
+        job.run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n0 = lib.ck_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        job.run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    peak, peak_kind = _peaks()
+    ms_step = ms / args.steps
+    achieved = bytes_unit * per_step / (ms_step / 1000.0) / 1e9
+    extra = {}
+    if wl.kind == "bsgs" and rank == 0:
+        from paper_2112_06396_b200.digest import digest
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+        extra["parity_vs_reference_digest"] = (
+            digest(job.out[0].cpu().numpy(), job.out[1].cpu().numpy()) == gold["C4_bsgs"]["digest"])
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"{unit} ({args.config})", "value": per_step * world * args.steps / (ms / 1000.0),
+            "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, generated on device)",
+            "config": {"workload": wl.desc, "units_per_gpu_per_step": per_step},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_unit": bytes_unit, "peak_kind": peak_kind},
+            "gpu_launches": lib.ck_launch_count() - n0, **extra}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -321,8 +390,14 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    args.batch_set = args.batch is not None
+    if args.batch is None:
+        args.batch = 64
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.config != "C3":
+        run_config(args, rank, world, local_rank)
         return
     run_ours(args, rank, world, local_rank)
 

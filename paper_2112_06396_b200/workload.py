@@ -92,3 +92,67 @@ class NttBatch:
         for inv in (0, 1):
             check(lib.ck_ntt(self.plan.h, ptr(self.x), ptr(self.idx), L, self.batch, L * n, inv,
                              stream_handle()), "ck_ntt")
+
+
+class BsgsWorkload:
+    """Config C4 on the device: one hoisted BSGS transform per run().
+
+    Inputs follow tests/golden/cases.py's C4 case exactly (same stream ids), so
+    the output digest can be checked against the reference golden.
+    """
+
+    def __init__(self, params, seed: int, baby: int = 16, giant: int = 8):
+        self.params, self.baby, self.giant = params, baby, giant
+        n, L = params.n_ring, params.limbs
+        full = params.full_moduli
+        raised = params.raised_moduli(L)
+        dn = len(params.digit_spans(L))
+        self.plan = plan_for(params)
+        dev = dict(dtype=torch.uint64, device="cuda")
+        self.a = torch.empty((L, n), **dev)
+        self.b = torch.empty((L, n), **dev)
+        k, q = _row_keys(seed, 0, synth.TAG_CT_A, params.chain)
+        fill_uniform(self.a, k, q, params.logn)
+        k, q = _row_keys(seed, 0, synth.TAG_CT_B, params.chain)
+        fill_uniform(self.b, k, q, params.logn)
+
+        def keys_for(rs):
+            kb = torch.empty((len(rs), dn, len(full), n), **dev)
+            ka = torch.empty((len(rs), dn, len(full), n), **dev)
+            kkb, qkb, kka, qka = [], [], [], []
+            for r in rs:
+                unit = 1000 + (r % (4 * n))
+                for j in range(dn):
+                    k, q = _row_keys(seed, unit, synth.TAG_KEY_B, full, j); kkb += k; qkb += q
+                    k, q = _row_keys(seed, unit, synth.TAG_KEY_A, full, j); kka += k; qka += q
+            fill_uniform(kb, kkb, qkb, params.logn)
+            fill_uniform(ka, kka, qka, params.logn)
+            return kb, ka
+
+        self.bkb, self.bka = keys_for([-k for k in range(1, baby + 1)])
+        self.gkb, self.gka = keys_for([-baby * j for j in range(1, giant + 1)])
+        self.diags = torch.empty((giant, baby, len(raised), n), **dev)
+        kk, qq = [], []
+        for j in range(1, giant + 1):
+            for kb_ in range(1, baby + 1):
+                k, q = _row_keys(seed, j, synth.TAG_DIAG, raised, kb_)
+                kk += k
+                qq += q
+        fill_uniform(self.diags, kk, qq, params.logn)
+        self.out = (torch.empty((L - 1, n), **dev), torch.empty((L - 1, n), **dev))
+        nbytes = load().ck_bsgs_workspace_bytes(self.plan.h, L, baby, giant)
+        self.ws = torch.empty(nbytes // 8, **dev)
+
+    def run(self) -> None:
+        ckks.bsgs_raw(self.params, self.a, self.b, self.bkb, self.bka, self.gkb, self.gka,
+                      self.diags, self.baby, self.giant, out=self.out, ws=self.ws)
+
+    def algorithmic_bytes(self) -> int:
+        """a, b; baby keys; diagonals; giant keys (at l-1); output."""
+        p = self.params
+        L, K = p.limbs, len(p.special)
+        beta = len(p.digit_spans(L))
+        beta1 = len(p.digit_spans(L - 1))
+        limbs = (2 * L + self.baby * 2 * beta * (L + K) + self.giant * self.baby * (L + K)
+                 + self.giant * 2 * beta1 * (L - 1 + K) + 2 * (L - 1))
+        return limbs * p.n_ring * 8
