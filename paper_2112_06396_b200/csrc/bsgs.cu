@@ -15,6 +15,9 @@ namespace ck {
 constexpr int kDiagThreads = 256;
 constexpr int kMaxBaby = 32;
 
+// MB: compile-time upper bound on the baby count (fully unrolled, baby
+// inputs stay in registers; entries k >= baby are never touched).
+template <int MB>
 __global__ void __launch_bounds__(kDiagThreads) diag_mac_kernel(DiagArgs a) {
   const int n = 1 << a.logn;
   const int c = blockIdx.x * kDiagThreads + threadIdx.x;
@@ -23,9 +26,10 @@ __global__ void __launch_bounds__(kDiagThreads) diag_mac_kernel(DiagArgs a) {
   if (c >= n) return;
   const PrimeConst& P = a.pc[a.prime[i]];
   const long long rowN = (long long)a.R << a.logn;
-  u64 x[kMaxBaby];
+  u64 x[MB];
 #pragma unroll
-  for (int k = 0; k < kMaxBaby; ++k) {
+  for (int k = 0; k < MB; ++k) {
+    x[k] = 0;
     if (k < a.baby) {
       u64 v = a.uv[(2LL * k + w) * rowN + ((long long)i << a.logn) + c];
       if (w == 1 && i < a.l) {
@@ -41,12 +45,12 @@ __global__ void __launch_bounds__(kDiagThreads) diag_mac_kernel(DiagArgs a) {
     const u64* d = a.diags + (long long)j * a.baby * rowN + ((long long)i << a.logn) + c;
     u64 y = 0;
 #pragma unroll
-    for (int k0 = 0; k0 < kMaxBaby; k0 += 8) {
-      if (k0 >= a.baby) break;
+    for (int k0 = 0; k0 < MB; k0 += 8) {
+      if (k0 >= a.baby) continue;
       Acc3 s;
       acc3_zero(s);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
+      for (int kk = 0; kk < 8 && k0 + kk < MB; ++kk) {
         const int k = k0 + kk;
         if (k < a.baby) {
           const u64 m = __ldg(d + k * rowN);
@@ -63,7 +67,11 @@ int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
   if (a.baby < 1 || a.baby > kMaxBaby || a.giant < 1) return CK_ERR_ARG;
   count_launches(1);
   const int n = 1 << a.logn;
-  diag_mac_kernel<<<dim3((n + kDiagThreads - 1) / kDiagThreads, a.R, 2), kDiagThreads, 0, st>>>(a);
+  const dim3 grid((n + kDiagThreads - 1) / kDiagThreads, a.R, 2);
+  if (a.baby <= 4) diag_mac_kernel<4><<<grid, kDiagThreads, 0, st>>>(a);
+  else if (a.baby <= 8) diag_mac_kernel<8><<<grid, kDiagThreads, 0, st>>>(a);
+  else if (a.baby <= 16) diag_mac_kernel<16><<<grid, kDiagThreads, 0, st>>>(a);
+  else diag_mac_kernel<32><<<grid, kDiagThreads, 0, st>>>(a);
   return (int)cudaGetLastError();
 }
 
