@@ -87,10 +87,10 @@ __global__ void __launch_bounds__(kBcThreads) bconv_kernel(BconvArgs a) {
       const uint4 t = Ts[i * nd + j];
 #pragma unroll
       for (int c = 0; c < kBcCpt; ++c) {
-        lo[c] += (u64)v0[c][i] * t.x;
-        lo[c] += (u64)v1[c][i] * t.z;
-        hi[c] += (u64)v0[c][i] * t.y;
-        hi[c] += (u64)v1[c][i] * t.w;
+        lo[c] = madw(v0[c][i], t.x, lo[c]);
+        lo[c] = madw(v1[c][i], t.z, lo[c]);
+        hi[c] = madw(v0[c][i], t.y, hi[c]);
+        hi[c] = madw(v1[c][i], t.w, hi[c]);
       }
       if ((i & 7) == 7 || i == NS - 1) {  // chunk of <= 8 sources: reduce
 #pragma unroll

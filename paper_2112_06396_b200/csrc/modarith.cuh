@@ -61,15 +61,23 @@ CK_D u64 mulmod(u64 a, u64 b, const PrimeConst& P) {
 // 30-bit split accumulators: for a, b < 2^60 the product is
 //   a0 b0 + (a0 b1 + a1 b0) 2^30 + a1 b1 2^60,  pieces < 2^30.
 // Up to 8 products accumulate without overflow (mid term: 16 partials < 2^64).
+// acc + (u64)a * b with a, b < 2^32: exactly one IMAD.WIDE.U32 (plain C++
+// `acc += (u64)a * b` makes nvcc emit extra zero-high-word adds).
+CK_D u64 madw(u32 a, u32 b, u64 acc) {
+  u64 d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(acc));
+  return d;
+}
+
 struct Acc3 {
   u64 lo, mid, hi;
 };
 CK_D void acc3_zero(Acc3& s) { s.lo = s.mid = s.hi = 0; }
 CK_D void acc3_mac(Acc3& s, u32 a0, u32 a1, u32 b0, u32 b1) {
-  s.lo += (u64)a0 * b0;
-  s.mid += (u64)a0 * b1;
-  s.mid += (u64)a1 * b0;
-  s.hi += (u64)a1 * b1;
+  s.lo = madw(a0, b0, s.lo);
+  s.mid = madw(a0, b1, s.mid);
+  s.mid = madw(a1, b0, s.mid);
+  s.hi = madw(a1, b1, s.hi);
 }
 CK_D u32 lo30(u64 x) { return (u32)x & 0x3fffffffu; }
 CK_D u32 hi30(u64 x) { return (u32)(x >> 30); }

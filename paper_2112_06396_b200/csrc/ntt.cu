@@ -11,7 +11,7 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 // ------------------------------------------------------------ column phase
 // grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(kTC * (1 << P1) / kE)
+__global__ void __launch_bounds__(kTC * (1 << P1) / kE, 4)
 ntt_col_kernel(NttArgs a) {
   constexpr int S = 1 << P1;
   constexpr int G = S / kE;
@@ -75,7 +75,7 @@ struct RowCfg {
 };
 
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;
