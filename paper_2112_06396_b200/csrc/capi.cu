@@ -352,13 +352,15 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   a.itw = p->d_itw;
   a.scale = scale;
   a.batch_stride = bstride;
+  a.src = nullptr;
+  a.src_batch_stride = 0;
   a.logn = p->logn;
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
 
 int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* off,
               const ulonglong2* scale, int jobs, int batch, long long bstride, bool inv,
-              int phase, cudaStream_t st) {
+              int phase, cudaStream_t st, const u64* src = nullptr, long long src_bstride = 0) {
   ck::NttArgs a;
   a.data = base;
   a.prime_idx = prime;
@@ -368,6 +370,8 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   a.itw = p->d_itw;
   a.scale = scale;
   a.batch_stride = bstride;
+  a.src = src;
+  a.src_batch_stride = src_bstride;
   a.logn = p->logn;
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
@@ -511,8 +515,8 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   const long long N = p->n, l = level, R = t.R;
   const long long dig_b = (long long)t.beta * R * N;
   // ---- ModUp: INTT of a (row then column phase, ihat*n^-1 folded), BC, fwd column phase
-  CK_TRY((int)cudaMemcpyAsync(w.tmp, a_src, sizeof(u64) * B * l * N, cudaMemcpyDeviceToDevice, st));
-  CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, nullptr, level, B, l * N, true, 2, st));
+  CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, nullptr, level, B, l * N, true, 2, st,
+                   a_src, l * N));  // row phase reads the ciphertext directly
   CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, t.d_modup_scale, level, B, l * N, true, 1,
                    st));
   for (int d = 0; d < t.beta; ++d)

@@ -85,19 +85,22 @@ ntt_row_kernel(NttArgs a) {
   const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
   const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
   u64* base = a.data + job_offset(a, job, blockIdx.y);
+  const u64* ibase = a.src ? a.src + ((long long)job << a.logn) + (long long)blockIdx.y * a.src_batch_stride
+                           : base;  // out-of-place input (e.g. ModUp reads the ciphertext directly)
   const int rl = threadIdx.x / R::G, g = threadIdx.x % R::G;
   const int row = blockIdx.x * R::TR + rl;
   u64* rowp = base + ((long long)row << P2);
+  const u64* irowp = ibase + ((long long)row << P2);
   u64* srow = sm + rl * R::RS;
   const int jbase = row << P2;
   u64 x[kE];
   auto sidx = [](int s) { return s + (s >> 4); };
   if (!INV) {
 #pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = rowp[sub_index<P2, 0, INV>(g, r)];
+    for (int r = 0; r < kE; ++r) x[r] = irowp[sub_index<P2, 0, INV>(g, r)];
   } else {
     // pass 0 of the inverse reads contiguous runs: stage through smem
-    u64* tile = base + ((long long)blockIdx.x * R::TR << P2);
+    const u64* tile = ibase + ((long long)blockIdx.x * R::TR << P2);
     for (int i = threadIdx.x; i < R::TR * R::S; i += blockDim.x)
       sm[(i >> P2) * R::RS + sidx(i & (R::S - 1))] = tile[i];
     __syncthreads();

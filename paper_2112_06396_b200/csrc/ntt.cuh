@@ -35,6 +35,8 @@ struct NttArgs {
   const ulonglong2* itw;       // [prime][N] inverse
   const ulonglong2* scale;     // per job {s, s_shoup} applied after INTT (nullable: n^-1)
   long long batch_stride;      // elements between batch items (grid.z)
+  const u64* src;              // row kernels: read input from here (nullable: in place)
+  long long src_batch_stride;  //   with this batch stride (rows at job*N)
   int logn;
 };
 
