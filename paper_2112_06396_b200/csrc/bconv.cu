@@ -30,8 +30,15 @@ struct BcDst {
   u64 p, bar, c30, c30p;
 };
 
+// Several independent conversions (e.g. the beta ModUp digits) share one
+// launch: grid.y selects the group.
+struct BconvGroups {
+  BconvArgs g[kMaxBcGroups];
+};
+
 template <int NS>
-__global__ void __launch_bounds__(kBcThreads) bconv_kernel(BconvArgs a) {
+__global__ void __launch_bounds__(kBcThreads) bconv_kernel(const __grid_constant__ BconvGroups G) {
+  const BconvArgs& a = G.g[blockIdx.y];
   extern __shared__ __align__(16) unsigned char bc_smem[];
   const int nd = a.nd;
   uint4* Ts = (uint4*)bc_smem;                         // [NS][nd]
@@ -116,35 +123,52 @@ __global__ void __launch_bounds__(kBcThreads) bconv_kernel(BconvArgs a) {
 }
 
 template <int NS>
-static void launch_ns(const BconvArgs& a, int batch, cudaStream_t st) {
-  const int n = 1 << a.logn;
+static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
+  const int n = 1 << G.g[0].logn;
   const int per = kBcThreads * kBcCpt;
-  const dim3 grid((n + per - 1) / per, 1, batch);
-  const size_t smem = (size_t)NS * a.nd * sizeof(uint4) + a.nd * sizeof(BcDst) +
-                      (a.centered ? (size_t)a.nd * (a.ns + 1) * sizeof(u64) : 0);
+  const dim3 grid((n + per - 1) / per, ng, batch);
+  size_t smem = 0;
+  for (int i = 0; i < ng; ++i) {
+    const BconvArgs& a = G.g[i];
+    const size_t s = (size_t)NS * a.nd * sizeof(uint4) + a.nd * sizeof(BcDst) +
+                     (a.centered ? (size_t)a.nd * (a.ns + 1) * sizeof(u64) : 0);
+    smem = s > smem ? s : smem;
+  }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(bconv_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  bconv_kernel<NS><<<grid, kBcThreads, smem, st>>>(a);
+  bconv_kernel<NS><<<grid, kBcThreads, smem, st>>>(G);
+}
+
+int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st) {
+  if (ng <= 0 || batch <= 0) return 0;
+  if (ng > kMaxBcGroups) return CK_ERR_ARG;
+  BconvGroups G;
+  int ns = 0;
+  for (int i = 0; i < ng; ++i) {
+    if (gs[i].nd <= 0 || gs[i].ns < 1) return CK_ERR_ARG;
+    G.g[i] = gs[i];
+    ns = gs[i].ns > ns ? gs[i].ns : ns;
+  }
+  count_launches(1);
+  // smallest compiled source count >= ns (extra source rows are zero)
+  if (ns <= 1) launch_ns<1>(G, ng, batch, st);
+  else if (ns <= 2) launch_ns<2>(G, ng, batch, st);
+  else if (ns <= 4) launch_ns<4>(G, ng, batch, st);
+  else if (ns <= 8) launch_ns<8>(G, ng, batch, st);
+  else if (ns <= 9) launch_ns<9>(G, ng, batch, st);
+  else if (ns <= 10) launch_ns<10>(G, ng, batch, st);
+  else if (ns <= 12) launch_ns<12>(G, ng, batch, st);
+  else if (ns <= 16) launch_ns<16>(G, ng, batch, st);
+  else if (ns <= 24) launch_ns<24>(G, ng, batch, st);
+  else if (ns <= 32) launch_ns<32>(G, ng, batch, st);
+  else if (ns <= 48) launch_ns<48>(G, ng, batch, st);
+  else return CK_ERR_ARG;
+  return (int)cudaGetLastError();
 }
 
 int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st) {
   if (a.nd <= 0 || batch <= 0) return 0;
-  count_launches(1);
-  // smallest compiled source count >= ns (extra source rows are zero)
-  if (a.ns < 1) return CK_ERR_ARG;
-  if (a.ns <= 1) launch_ns<1>(a, batch, st);
-  else if (a.ns <= 2) launch_ns<2>(a, batch, st);
-  else if (a.ns <= 4) launch_ns<4>(a, batch, st);
-  else if (a.ns <= 8) launch_ns<8>(a, batch, st);
-  else if (a.ns <= 9) launch_ns<9>(a, batch, st);
-  else if (a.ns <= 10) launch_ns<10>(a, batch, st);
-  else if (a.ns <= 12) launch_ns<12>(a, batch, st);
-  else if (a.ns <= 16) launch_ns<16>(a, batch, st);
-  else if (a.ns <= 24) launch_ns<24>(a, batch, st);
-  else if (a.ns <= 32) launch_ns<32>(a, batch, st);
-  else if (a.ns <= 48) launch_ns<48>(a, batch, st);
-  else return CK_ERR_ARG;
-  return (int)cudaGetLastError();
+  return launch_bconv_groups(&a, 1, batch, st);
 }
 
 }  // namespace ck

@@ -376,8 +376,8 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
 
-int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
-              u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st) {
+ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
+                         u64* out, long long out_batch, bool prescale) {
   ck::BconvArgs a;
   a.in = in;
   a.in_batch = in_batch;
@@ -396,6 +396,12 @@ int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_
   a.nd = bc->nd;
   a.logn = p->logn;
   a.centered = bc->centered;
+  return a;
+}
+
+int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
+              u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st) {
+  const ck::BconvArgs a = bconv_args(p, bc, in, in_batch, out, out_batch, prescale);
   return ck::launch_bconv(a, batch, st);
 }
 
@@ -519,9 +525,17 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
                    a_src, l * N));  // row phase reads the ciphertext directly
   CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, t.d_modup_scale, level, B, l * N, true, 1,
                    st));
-  for (int d = 0; d < t.beta; ++d)
-    CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
-                     false, B, st));
+  if (t.beta <= ck::kMaxBcGroups) {  // all digits' conversions in one launch
+    ck::BconvArgs gs[ck::kMaxBcGroups];
+    for (int d = 0; d < t.beta; ++d)
+      gs[d] = bconv_args(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
+                         false);
+    CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
+  } else {
+    for (int d = 0; d < t.beta; ++d)
+      CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
+                       false, B, st));
+  }
   CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
                    dig_b, false, 1, st));
   // ---- row phase + automorph + KSKIP (+ INTT row phase of the special rows)
@@ -562,7 +576,7 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
                    st));
   CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false, 1,
                    st));
-  // ---- fwd row phase of the converted rows fused with the epilogue
+  // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
   ck::MdRowArgs ma;
   ma.prime = m.d_keep_prime;
   ma.pinv = m.d_pinv;
@@ -573,20 +587,16 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ma.x_batch = 2 * R * N;
   ma.conv = w.conv;
   ma.conv_batch = 2 * l * N;
-  ma.addend = nullptr;
-  ma.addend_batch = 0;
-  ma.out = out_a;
-  ma.out_batch = l * N;
-  ma.galois = nullptr;
-  ma.galois_t = 1;
-  CK_TRY(ck::launch_md_row(ma, level, B, st));
-  ma.x = w.uv + R * N;
-  ma.conv = w.conv + l * N;
   ma.addend = b_add;
   ma.addend_batch = l * N;
-  ma.out = out_b;
+  ma.out = out_a;
+  ma.out_batch = l * N;
   ma.galois = egal;
   ma.galois_t = egt;
+  ma.pair = 1;
+  ma.x_w = R * N;
+  ma.conv_w = l * N;
+  ma.out2 = out_b;
   return ck::launch_md_row(ma, level, B, st);
 }
 

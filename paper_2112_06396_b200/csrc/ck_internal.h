@@ -64,6 +64,11 @@ struct MdRowArgs {
   const u64* galois;
   u64 galois_t;
   int logn;
+  // pair mode: grid.y = 2*batch; odd items are the second polynomial at
+  // x + x_w, conv + conv_w, written to out2 with the addend (u/v of ModDown)
+  int pair;
+  long long x_w, conv_w;
+  u64* out2;
 };
 int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st);
 
@@ -100,6 +105,8 @@ struct BconvArgs {
   int ns, nd, logn, centered;
 };
 int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st);
+constexpr int kMaxBcGroups = 8;
+int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st);
 
 // Key-switching inner product with a fused eval-domain automorphism.
 struct KskipArgs {

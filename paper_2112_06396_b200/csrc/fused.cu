@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
   constexpr int LOGN = P1 + P2;
   __shared__ u64 stage[F::TR * F::RS];
   const int j = blockIdx.z;  // grid (row tile, batch, limb): twiddle reuse across the batch
-  const long long b = blockIdx.y;
+  const int w = a.pair ? (blockIdx.y & 1) : 1;   // w = 1: the polynomial that gets the addend
+  const long long b = a.pair ? (blockIdx.y >> 1) : blockIdx.y;
   const int prime = a.prime[j];
   const PrimeConst& P = a.pc[prime];
   const u64 q = P.q, two_q = P.two_q;
@@ -357,8 +358,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
   u64* srow = stage + rl * F::RS;
   const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
   const long long ro = ((long long)j << LOGN) + ((long long)r << P2);
-  const u64* conv = a.conv + b * a.conv_batch + ro;
-  const u64* x = a.x + b * a.x_batch + ro;
+  const u64* conv = a.conv + b * a.conv_batch + ro + (a.pair && w ? a.conv_w : 0);
+  const u64* x = a.x + b * a.x_batch + ro + (a.pair && w ? a.x_w : 0);
   u64 y[kE];
 #pragma unroll
   for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
     const int c = sub_index<P2, 0, false>(g, k);
     o[k] = shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
   }
-  if (a.addend) {
+  if (a.addend && w) {
     const u64 t = a.galois ? a.galois[b] : a.galois_t;
     const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
     const u64* add = a.addend + b * a.addend_batch + ((long long)j << LOGN) + ((long long)sr << P2);
@@ -392,7 +393,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT) md_row_kernel(MdRowArgs a) {
       o[k] = addmod(o[k], srow[sidx(sc)], q);
     }
   }
-  u64* out = a.out + b * a.out_batch + ((long long)j << LOGN) + ((long long)r << P2);
+  u64* out = (a.pair && w ? a.out2 : a.out) + b * a.out_batch + ((long long)j << LOGN) +
+             ((long long)r << P2);
 #pragma unroll
   for (int k = 0; k < kE; ++k) out[sub_index<P2, 0, false>(g, k)] = o[k];
 }
@@ -439,7 +441,7 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
 template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
-  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, batch, rows), F::NT, 0, st>>>(a);
+  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, batch * (a.pair ? 2 : 1), rows), F::NT, 0, st>>>(a);
   return 0;
 }
 
