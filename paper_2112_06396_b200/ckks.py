@@ -449,3 +449,67 @@ def rotate_batch(params: CkksParams, a: torch.Tensor, b: torch.Tensor, key_b: to
 
 def automorph(x: RnsPoly, t: int) -> RnsPoly:
     return RnsPoly(x.moduli, automorph_rows(x.data, t, x.moduli), x.rep)
+
+
+class HostRotationPipeline:
+    """Batched rotation key-switches on HOST (pinned) buffers -- the entry point
+    for callers whose ciphertexts and evaluation keys live in host memory.
+
+    The batch is cut into chunks; chunk c+1's host->device copy and chunk c-1's
+    device->host copy run on their own streams while chunk c computes, so the
+    PCIe transfers (8 GB of keys per 64 C3 rotations) overlap the key-switch.
+    """
+
+    def __init__(self, params: CkksParams, batch: int, chunk: int = 8):
+        self.params = params
+        self.plan = plan_for(params)
+        self.batch, self.chunk = batch, min(chunk, batch)
+        n, L = params.n_ring, params.limbs
+        dn = len(params.digit_spans(L))
+        full = len(params.full_moduli)
+        dev = dict(dtype=torch.uint64, device="cuda")
+        C = self.chunk
+        self.buf = [dict(a=torch.empty((C, L, n), **dev), b=torch.empty((C, L, n), **dev),
+                         kb=torch.empty((C, dn, full, n), **dev), ka=torch.empty((C, dn, full, n), **dev),
+                         oa=torch.empty((C, L, n), **dev), ob=torch.empty((C, L, n), **dev))
+                    for _ in range(2)]
+        self.ws = self.plan.workspace(L, C, "hostpipe")
+        self.s_h2d = torch.cuda.Stream()
+        self.s_d2h = torch.cuda.Stream()
+        self.s_comp = torch.cuda.Stream()
+
+    def run(self, a, b, key_b, key_a, galois, out_a, out_b) -> None:
+        """a, b, key_b, key_a, out_a, out_b: pinned host tensors ([B][...]);
+        galois: (B,) uint64 DEVICE tensor.  Stream-ordered after the current stream."""
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s in (self.s_h2d, self.s_d2h, self.s_comp):
+            s.wait_event(start)
+        loaded = [torch.cuda.Event() for _ in range(2)]
+        computed = [torch.cuda.Event() for _ in range(2)]
+        freed = [None, None]
+        for ci, c0 in enumerate(range(0, self.batch, self.chunk)):
+            s = ci % 2
+            cc = min(self.chunk, self.batch - c0)
+            bf = self.buf[s]
+            with torch.cuda.stream(self.s_h2d):
+                if freed[s] is not None:
+                    self.s_h2d.wait_event(freed[s])
+                for name, src in (("a", a), ("b", b), ("kb", key_b), ("ka", key_a)):
+                    bf[name][:cc].copy_(src[c0:c0 + cc], non_blocking=True)
+                loaded[s].record(self.s_h2d)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(loaded[s])
+                rotate_batch(self.params, bf["a"][:cc], bf["b"][:cc], bf["kb"][:cc], bf["ka"][:cc],
+                             galois[c0:c0 + cc], bf["oa"][:cc], bf["ob"][:cc], self.ws)
+                computed[s].record(self.s_comp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(computed[s])
+                out_a[c0:c0 + cc].copy_(bf["oa"][:cc], non_blocking=True)
+                out_b[c0:c0 + cc].copy_(bf["ob"][:cc], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_d2h)
+                freed[s] = ev
+        for s in (self.s_h2d, self.s_d2h, self.s_comp):
+            cur.wait_stream(s)

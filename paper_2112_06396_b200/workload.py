@@ -64,6 +64,11 @@ class RotationBatch:
         ckks.rotate_batch(self.params, self.a, self.b, self.key_b, self.key_a, self.galois,
                           self.out_a, self.out_b, self.ws)
 
+    def release_inputs(self) -> None:
+        """Drop the device-resident keys (8 GB at C3) -- outputs are kept."""
+        self.key_b = self.key_a = None
+        torch.cuda.empty_cache()
+
     def input_bytes(self) -> int:
         return sum(t.numel() * 8 for t in (self.a, self.b, self.key_b, self.key_a))
 
