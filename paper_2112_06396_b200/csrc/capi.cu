@@ -153,6 +153,9 @@ struct ck_plan {
   PrimeConst* d_pc = nullptr;
   ulonglong2* d_tw = nullptr;
   ulonglong2* d_itw = nullptr;
+  Tw4* d_ctw = nullptr;   // column-phase twiddles, FP64-assisted form [prime][2^P1]
+  Tw4* d_citw = nullptr;
+  bool fp_ntt = false;    // CKB200_FPNTT=1: FP64-assisted column twiddles (measured slower)
   std::vector<LevelTab> lv;  // index = level
   std::vector<void*> allocs;
   std::vector<ck_bconv*> bcs;
@@ -188,6 +191,7 @@ PrimeConst make_pc(u64 q, int logn) {
   P.r64p = shoup_h(P.r64, q);
   P.ninv = invmod_h(((u64)1 << logn) % q, q);
   P.ninvp = shoup_h(P.ninv, q);
+  P.nq = (u64)0 - q;
   return P;
 }
 
@@ -354,6 +358,8 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   a.batch_stride = bstride;
   a.src = nullptr;
   a.src_batch_stride = 0;
+  a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
+  a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
@@ -372,6 +378,8 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   a.batch_stride = bstride;
   a.src = src;
   a.src_batch_stride = src_bstride;
+  a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
+  a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
@@ -691,6 +699,29 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   p->d_pc = upload(p->allocs, pcs, &err);
   p->d_tw = upload(p->allocs, tw, &err);
   p->d_itw = upload(p->allocs, itw, &err);
+  if (log_n >= 12) {  // split transforms: column phase of 2^P1 points
+    const int p1 = log_n / 2, ct = 1 << p1;
+    std::vector<Tw4> ctw((size_t)np * ct), citw((size_t)np * ct);
+    auto mk = [](u64 w, u64 q) {
+      Tw4 t;
+      t.w0 = w;
+      t.w1 = mulmod_h(w, (u64)1 << 32, q);
+      t.f0 = (double)((long double)t.w0 / (long double)q);
+      t.f1 = (double)((long double)t.w1 / (long double)q);
+      return t;
+    };
+    for (int i = 0; i < np; ++i)
+      for (int k = 0; k < ct; ++k) {
+        ctw[(size_t)i * ct + k] = mk(tw[(size_t)i * N + k].x, p->mod[i]);
+        citw[(size_t)i * ct + k] = mk(itw[(size_t)i * N + k].x, p->mod[i]);
+      }
+    p->d_ctw = upload(p->allocs, ctw, &err);
+    p->d_citw = upload(p->allocs, citw, &err);
+  }
+  {
+    const char* e = getenv("CKB200_FPNTT");
+    p->fp_ntt = e && e[0] == '1';
+  }
   p->lv.resize(n_chain + 1);
   for (int l = 1; l <= n_chain && !err; ++l) err = build_level(p, l);
   if (err) { delete p; return err; }

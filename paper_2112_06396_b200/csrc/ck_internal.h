@@ -9,7 +9,11 @@
 #else
 typedef unsigned long long u64;
 struct PrimeConst {
-  u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, pad;
+  u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, nq;
+};
+struct Tw4 {
+  u64 w0, w1;
+  double f0, f1;
 };
 #endif
 

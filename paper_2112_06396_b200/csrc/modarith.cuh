@@ -25,7 +25,7 @@ struct PrimeConst {
   u64 c60, c60p;  // 2^60 mod q, Shoup companion
   u64 r64, r64p;  // 2^64 mod q, Shoup companion
   u64 ninv, ninvp;
-  u64 pad;
+  u64 nq;         // 2^64 - q
 };
 
 CK_D u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
@@ -134,3 +134,35 @@ CK_D void cp_async8(void* smem, const void* gmem) {
 CK_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 CK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---- FP64-assisted constant multiplication (NTT twiddles) ----
+// y * w mod q for any 64-bit y, split as y = y0 + y1 2^32:
+//   y w == y0 W0 + y1 W1 (mod q),  W0 = w, W1 = w 2^32 mod q.
+// Each 32-bit-quotient q_k = round(y_k * (W_k/q)) comes from ONE DFMA on the
+// otherwise idle FP64 pipe (magic-number rounding: fma(y_k, f_k, 1.5*2^52)
+// leaves round(y_k f_k) in the low mantissa bits; |q_k - y_k W_k/q| <= 1/2 +
+// 2^-21 since y_k < 2^32 is exact and f_k = fl(W_k/q)).  The residual
+// y0 W0 + y1 W1 - (q0 + q1) q is then exact mod 2^64 and lies in
+// (-(1+2^-20) q, (1+2^-20) q): adding 2q gives (0, 4q).  Integer work: four
+// 32x64 products (12 IMAD slots) instead of a 64x64 mulhi + two mullo (~19).
+struct Tw4 {
+  u64 w0, w1;
+  double f0, f1;
+};
+
+CK_D double u32_to_double(u32 v) {
+  return __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // exact
+}
+
+CK_D u64 fshoup4(u64 y, const Tw4& t, u64 q, u64 nq) {
+  const u32 y0 = (u32)y, y1 = (u32)(y >> 32);
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  const u32 q0 = (u32)__double2loint(__fma_rn(u32_to_double(y0), t.f0, M));
+  const u32 q1 = (u32)__double2loint(__fma_rn(u32_to_double(y1), t.f1, M));
+  u64 r = 2 * q;
+  r += (u64)y0 * t.w0;
+  r += (u64)q0 * nq;
+  r += (u64)y1 * t.w1;
+  r += (u64)q1 * nq;
+  return r;  // in (0, 4q)
+}

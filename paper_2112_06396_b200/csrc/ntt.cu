@@ -2,6 +2,8 @@
 #include "ntt.cuh"
 #include "ck_internal.h"
 
+#include <type_traits>
+
 namespace ck {
 
 CK_D long long job_offset(const NttArgs& a, int job, int bz) {
@@ -10,19 +12,23 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 
 // ------------------------------------------------------------ column phase
 // grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
-template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(kTC * (1 << P1) / kE, 4)
+template <int P1, int P2, bool INV, bool FP>
+__global__ void __launch_bounds__(kTC * (1 << P1) / kE, FP ? 3 : 4)
 ntt_col_kernel(NttArgs a) {
   constexpr int S = 1 << P1;
-  constexpr int G = S / kE;
   constexpr int NP = Sched<P1>::np;
   __shared__ u64 sm[S * kTC];
-  __shared__ ulonglong2 tws[S];
+  __shared__ typename std::conditional<FP, Tw4, ulonglong2>::type tws[S];
   const int job = blockIdx.y;
   const int prime = a.prime_idx[job];
-  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
-  const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
-  for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
+  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q, nq = a.pc[prime].nq;
+  if constexpr (FP) {
+    const Tw4* tw = (INV ? a.citw : a.ctw) + ((long long)prime << P1);
+    for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
+  } else {
+    const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
+    for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
+  }
   u64* base = a.data + job_offset(a, job, blockIdx.z);
   const int col = threadIdx.x % kTC, g = threadIdx.x / kTC;
   const int c = blockIdx.x * kTC + col;
@@ -30,7 +36,10 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
   for (int r = 0; r < kE; ++r) x[r] = base[((long long)sub_index<P1, 0, INV>(g, r) << P2) + c];
   __syncthreads();
-  run_pass<P1, 0, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
+#define CK_COL_PASS(PP)                                                        \
+  if constexpr (FP) run_pass_fp<P1, PP, INV, P1 + P2, P2>(x, g, c, tws, q, two_q, nq); \
+  else run_pass<P1, PP, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
+  CK_COL_PASS(0)
   if constexpr (NP > 1) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) sm[sub_index<P1, 0, INV>(g, r) * kTC + col] = x[r];
@@ -38,7 +47,7 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 1, INV>(g, r) * kTC + col];
     if (!INV) fwd_fold(x, q << 3);
-    run_pass<P1, 1, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
+    CK_COL_PASS(1)
   }
   if constexpr (NP > 2) {
     __syncthreads();
@@ -48,8 +57,9 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 2, INV>(g, r) * kTC + col];
     if (!INV) fwd_fold(x, q << 3);
-    run_pass<P1, 2, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
+    CK_COL_PASS(2)
   }
+#undef CK_COL_PASS
   static_assert(NP <= 3, "sub-transform too large");
   if (INV) {
     // end of the inverse: scale by n^-1 (times the optional extra constant)
@@ -199,12 +209,19 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
   const dim3 grow((1 << P1) / R::TR, batch, jobs), brow(R::TR * R::G);
   const bool col = phase != 2, row = phase != 1;
   count_launches((int)col + (int)row);
+  const bool fp = a.ctw != nullptr;
   if (!inv) {
-    if (col) ntt_col_kernel<P1, P2, false><<<gcol, bcol, 0, st>>>(a);
+    if (col) {
+      if (fp) ntt_col_kernel<P1, P2, false, true><<<gcol, bcol, 0, st>>>(a);
+      else ntt_col_kernel<P1, P2, false, false><<<gcol, bcol, 0, st>>>(a);
+    }
     if (row) ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
   } else {
     if (row) ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
-    if (col) ntt_col_kernel<P1, P2, true><<<gcol, bcol, 0, st>>>(a);
+    if (col) {
+      if (fp) ntt_col_kernel<P1, P2, true, true><<<gcol, bcol, 0, st>>>(a);
+      else ntt_col_kernel<P1, P2, true, false><<<gcol, bcol, 0, st>>>(a);
+    }
   }
 }
 
