@@ -148,7 +148,8 @@ struct ck_plan {
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
   int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
   int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
-  int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = whole batch)
+  int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
+  int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   ulonglong2* d_tw = nullptr;
@@ -652,6 +653,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     p->ks_ws = wsv ? atoi(wsv) : 0;
     const char* c = getenv("CKB200_CHUNK");
     if (c) p->chunk = atoi(c);
+    const char* ns = getenv("CKB200_STREAMS");
+    if (ns) p->nstreams = atoi(ns);
   }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
@@ -902,22 +905,52 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
     kgal = nullptr;
   }
   if (ck::fused_supported(p->logn) && p->fused) {
-    // Optional chunking (CKB200_CHUNK): run the pipeline on `chunk`
-    // key-switches at a time with the same workspace addresses so the
-    // intermediates stay L2-resident.  Measured slower than one pass over the
-    // whole batch (the kernels are INT-bound and want the parallelism), so the
-    // default is 0 = whole batch; see DESIGN.md section 5.
-    const int C = p->chunk > 0 ? std::min(p->chunk, batch) : batch;
+    // Chunked software pipeline: the batch is cut into chunks issued
+    // round-robin on `nstreams` internal streams (forked from / joined to the
+    // caller's stream), each with its own slice of the workspace, so kernels
+    // of different chunks (compute-bound NTT/BC vs. key-streaming KSKIP) can
+    // run concurrently.  Defaults from CKB200_CHUNK / CKB200_STREAMS.
+    const int NS = std::max(1, std::min(p->nstreams, batch));
+    int C = p->chunk > 0 ? std::min(p->chunk, batch) : batch;
+    if (NS > 1 && p->chunk <= 0) C = (batch + 2 * NS - 1) / (2 * NS);
     const long long kbatch = (long long)p->key_digits * (p->L + p->K) * N;
     const u64* egal = mode == 1 ? nullptr : galois;
-    for (int c0 = 0; c0 < batch; c0 += C) {
-      const int cc = std::min(C, batch - c0);
-      CK_TRY(rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N, key_b + c0 * kbatch,
-                          key_a + c0 * kbatch, kgt, kgal ? kgal + c0 : nullptr, egt,
-                          egal ? egal + c0 : nullptr, out_a + c0 * l * N, out_b + c0 * l * N, w,
-                          cc, st));
+    if (NS == 1) {
+      for (int c0 = 0; c0 < batch; c0 += C) {
+        const int cc = std::min(C, batch - c0);
+        CK_TRY(rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N,
+                            key_b + c0 * kbatch, key_a + c0 * kbatch, kgt,
+                            kgal ? kgal + c0 : nullptr, egt, egal ? egal + c0 : nullptr,
+                            out_a + c0 * l * N, out_b + c0 * l * N, w, cc, st));
+      }
+      return 0;
     }
-    return 0;
+    std::vector<cudaStream_t> ss(NS);
+    std::vector<cudaEvent_t> ev(NS + 1);
+    for (int i = 0; i < NS; ++i) CK_TRY((int)cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking));
+    for (int i = 0; i <= NS; ++i) CK_TRY((int)cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    CK_TRY((int)cudaEventRecord(ev[NS], st));
+    // per-stream workspace slices (regions sized for C items each; C*NS <= batch)
+    const size_t slice = ck_workspace_bytes(p, level, C) / sizeof(u64);
+    int rc = 0;
+    for (int i = 0; i < NS && !rc; ++i) rc = (int)cudaStreamWaitEvent(ss[i], ev[NS], 0);
+    for (int ci = 0, c0 = 0; c0 < batch && !rc; ++ci, c0 += C) {
+      const int cc = std::min(C, batch - c0);
+      const int si = ci % NS;
+      const Ws wsi = ws_layout(p, level, C, (u64*)workspace + (mode == 1 ? 0 : si * slice) +
+                                                (mode == 1 ? 2LL * batch * l * N + si * slice : 0));
+      rc = rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N, key_b + c0 * kbatch,
+                        key_a + c0 * kbatch, kgt, kgal ? kgal + c0 : nullptr, egt,
+                        egal ? egal + c0 : nullptr, out_a + c0 * l * N, out_b + c0 * l * N, wsi,
+                        cc, ss[si]);
+    }
+    for (int i = 0; i < NS; ++i) {
+      cudaEventRecord(ev[i], ss[i]);
+      cudaStreamWaitEvent(st, ev[i], 0);
+    }
+    for (int i = 0; i < NS; ++i) cudaStreamDestroy(ss[i]);
+    for (int i = 0; i <= NS; ++i) cudaEventDestroy(ev[i]);
+    return rc;
   }
   CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
   // uv: [B][2][R][N]
