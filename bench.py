@@ -54,6 +54,22 @@ def ks_bytes(params, limbs=None) -> int:
     return 8 * params.n_ring * (l + l + 2 * beta * (l + K) + 2 * l)
 
 
+def int_slots_per_ks(params, limbs=None) -> float:
+    """Analytic IMAD-pipe slots of one rotation key-switch:
+    160 limb NTTs x N/2 log N Shoup butterflies (18 slots), base conversions
+    (8 slots per source MAC + 26 per reduction), KSKIP (6 MACs + 2 reductions)."""
+    l = params.limbs if limbs is None else limbs
+    K = len(params.special)
+    spans = params.digit_spans(l)
+    beta, R, n, logn = len(spans), l + K, params.n_ring, params.logn
+    ntt_limbs = l + sum(R - (hi - lo) for lo, hi in spans) + 2 * K + 2 * l
+    bfly = ntt_limbs * (n // 2) * logn * 18
+    bc = sum((R - (hi - lo)) * ((hi - lo) * 8 + 26) for lo, hi in spans) * n
+    bc += 2 * l * (K * 8 + 26) * n
+    ks = R * n * (2 * beta * 8 + 2 * 28)
+    return float(bfly + bc + ks)
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -247,6 +263,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "kernel": "ck_rotate pipeline (batched key-switch, all launches of one step)",
                 "algorithmic_bytes_per_unit": bytes_ks, "units_per_launch": B,
                 "peak_kind": peak_kind}
+    # The path is INT-issue bound: report the IMAD-pipe
+    # roofline too.  Slots = analytic IMAD-pipe slots per key-switch; peak =
+    # 64 IMAD slots/clk/SM (profiles/r01_microbench_int.txt) x SMs x clock.
+    props = torch.cuda.get_device_properties(local_rank)
+    clk_mhz = clocks.get("sm_mhz") or 1965.0
+    slots = int_slots_per_ks(p)
+    int_peak = props.multi_processor_count * 64 * clk_mhz * 1e6
+    int_ach = slots * B / (ms_step / 1000.0)
+    roofline["int_pipe"] = {"bound": "imad", "achieved_slots_per_s": int_ach, "peak_slots_per_s": int_peak,
+                            "frac": int_ach / int_peak, "slots_per_unit": slots,
+                            "note": "18 IMAD slots per Shoup butterfly, 8 per 30-bit-split MAC, ~28 per reduction"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
