@@ -148,6 +148,7 @@ struct ck_plan {
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
   int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
   int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
+  int ks_intt_inline = 0;  // CKB200_KSINTT=1: special-row INTT row phase inside ks_row
   int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   std::vector<u64> mod, psi;
@@ -574,13 +575,13 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ka_.l = level;
   ka_.R = (int)R;
   ka_.logn = p->logn;
-  ka_.intt_special = 1;
+  ka_.intt_special = p->ks_intt_inline ? 1 : 0;
   ka_.dbg = p->ks_dbg;
   ka_.ws = p->ks_ws;
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
-                   true, 1, st));
+                   true, p->ks_intt_inline ? 1 : 0, st));
   CK_TRY(bconv_run(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv, l * N, false, 2 * B,
                    st));
   CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false, 1,
@@ -649,6 +650,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     p->fused = !(e && e[0] == '1');
     const char* d = getenv("CKB200_KSDBG");
     p->ks_dbg = d ? atoi(d) : 0;
+    const char* ki = getenv("CKB200_KSINTT");
+    p->ks_intt_inline = ki ? atoi(ki) : 0;
     const char* wsv = getenv("CKB200_KSWS");
     p->ks_ws = wsv ? atoi(wsv) : 0;
     const char* c = getenv("CKB200_CHUNK");
