@@ -145,6 +145,63 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsR
   u64* uo = ubase + ((long long)r << P2);
   u64* vo = uo + a.v_off;
   constexpr int ITER = (F::TR * F::S) / (2 * F::NT);
+  if constexpr (BETA > 0) {
+    // software-pipelined: the key vectors of iteration m+1 are in flight while
+    // iteration m multiplies (the MAC phase is otherwise load-latency bound)
+    ulonglong2 ya[BETA], yb[BETA];
+#pragma unroll
+    for (int d = 0; d < BETA; ++d) {
+      ya[d] = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + 2 * (int)threadIdx.x));
+      yb[d] = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + 2 * (int)threadIdx.x));
+    }
+#pragma unroll 1
+    for (int m = 0; m < ((a.dbg & 2) ? 0 : ITER); ++m) {
+      const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
+      ulonglong2 na[BETA], nb[BETA];
+      if (m + 1 < ITER) {
+#pragma unroll
+        for (int d = 0; d < BETA; ++d) {
+          na[d] = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + e + 2 * F::NT));
+          nb[d] = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + e + 2 * F::NT));
+        }
+      }
+      const int er = e >> P2, ec = e & (F::S - 1);
+      const int rr = blockIdx.x * F::TR + er;
+      int sc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        sc[h] = t == 1 ? ec + h
+                       : (int)(automorph_src(((u32)rr << P2) + ec + h, (u32)t, LOGN) & (F::S - 1));
+      Acc3 su[2], sv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc3_zero(su[h]);
+        acc3_zero(sv[h]);
+      }
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        const u64* drow = fsm + d * SLOT + er * F::RS;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const u64 x = drow[sidx(sc[h])];
+          const u64 ax = h ? ya[d].y : ya[d].x, bx = h ? yb[d].y : yb[d].x;
+          const u32 x0 = lo30(x), x1 = hi30(x);
+          acc3_mac(su[h], x0, x1, lo30(ax), hi30(ax));
+          acc3_mac(sv[h], x0, x1, lo30(bx), hi30(bx));
+        }
+      }
+      u64* uw = ubase + tile0 + e;
+      *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
+      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+      if (m + 1 < ITER) {
+#pragma unroll
+        for (int d = 0; d < BETA; ++d) {
+          ya[d] = na[d];
+          yb[d] = nb[d];
+        }
+      }
+    }
+  } else {
 #pragma unroll 2
   for (int m = 0; m < ((a.dbg & 2) ? 0 : ITER); ++m) {
     const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
@@ -163,7 +220,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsR
     }
 #pragma unroll
     for (int d = 0; d < NB; ++d) {
-      if (BETA == 0 && d >= beta) break;
+      if (d >= beta) break;
       const ulonglong2 ya = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + e));
       const ulonglong2 yb = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + e));
       const u64* drow = fsm + d * SLOT + er * F::RS;
@@ -179,6 +236,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsR
     u64* uw = ubase + tile0 + e;
     *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
     *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+  }
   }
   if (a.intt_special && i >= a.l && !(a.dbg & 4)) {
     // first half of ModDown's INTT on the special rows: re-read the row this
