@@ -37,7 +37,7 @@ struct BconvGroups {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kBcThreads) bconv_kernel(const __grid_constant__ BconvGroups G) {
+__global__ void __launch_bounds__(kBcThreads, 8) bconv_kernel(const __grid_constant__ BconvGroups G) {
   const BconvArgs& a = G.g[blockIdx.y];
   extern __shared__ __align__(16) unsigned char bc_smem[];
   const int nd = a.nd;
