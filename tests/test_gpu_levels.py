@@ -1,0 +1,101 @@
+"""Fused ck_rotate / conjugate at levels below the top, batched, and error behaviour.
+
+The reference supports key-switching at any level l <= L (ckks.py:421-465 use
+the digit spans and key rows of level l).  The oracle is pinned to the
+reference at the top level and at l-1 (tests/test_oracle_golden.py); here the
+GPU fused path is checked against it at several levels and batch sizes.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import ckks_np
+from paper_2112_06396_b200 import ckks, synth
+from paper_2112_06396_b200.device import plan_for, to_dev, to_host
+from paper_2112_06396_b200.params import CkksParams, config, prime_chain_below
+from paper_2112_06396_b200.rnspoly import RnsPoly
+
+pytestmark = pytest.mark.gpu
+
+
+def _params(logn, L, K, dnum, cb=54, sb=60):
+    chain, special = prime_chain_below(1 << logn, cb, L, sb, K)
+    return CkksParams(logn, chain, special, dnum, 2.0 ** 40, 1)
+
+
+@pytest.mark.parametrize("logn,L,K,dnum,level", [
+    (12, 6, 2, 3, 6), (12, 6, 2, 3, 5), (12, 6, 2, 3, 1), (13, 7, 3, 2, 4),
+    (14, 5, 5, 1, 3), (16, 24, 8, 3, 23), (16, 24, 8, 3, 17)])
+def test_fused_rotate_below_top_level(logn, L, K, dnum, level):
+    p = _params(logn, L, K, dnum)
+    a, b, kb, ka = synth.rotation_inputs(p, 77, 0, limbs=level)
+    k = 9
+    t = pow(5, k, 2 * p.n_ring)
+    want_a, want_b = ckks_np.rotate_galois(p, a, b, kb, ka, t)
+    ks = ckks.KeySet(p, None, None, rot={-k: ckks.SwitchingKey(p.full_moduli, kb, a=ka)})
+    ct = ckks.Ciphertext(RnsPoly(p.chain[:level], a, "eval"), RnsPoly(p.chain[:level], b, "eval"), 1.0)
+    out = ckks.rotate(p, ks, ct, -k)
+    assert np.array_equal(to_host(out.a.data), want_a)
+    assert np.array_equal(to_host(out.b.data), want_b)
+
+
+@pytest.mark.parametrize("batch", [1, 3, 5])
+def test_batched_rotate_distinct_galois_small_ring(batch):
+    p = _params(12, 6, 2, 3)
+    units = list(range(batch))
+    ins = [synth.rotation_inputs(p, 5, u) for u in units]
+    ks = [3 + 2 * u for u in units]
+    a = to_dev(np.stack([x[0] for x in ins])); b = to_dev(np.stack([x[1] for x in ins]))
+    kb = to_dev(np.stack([x[2] for x in ins])); ka = to_dev(np.stack([x[3] for x in ins]))
+    gal = torch.tensor(np.array([pow(5, k, 2 * p.n_ring) for k in ks], dtype=np.uint64), device="cuda")
+    oa, ob = torch.empty_like(a), torch.empty_like(b)
+    ckks.rotate_batch(p, a, b, kb, ka, gal, oa, ob)
+    for i, (x, k) in enumerate(zip(ins, ks)):
+        wa, wb = ckks_np.rotate_galois(p, *x, pow(5, k, 2 * p.n_ring))
+        assert np.array_equal(to_host(oa[i]), wa) and np.array_equal(to_host(ob[i]), wb)
+
+
+def test_conjugate_below_top_level():
+    p = _params(13, 6, 2, 3)
+    level = 4
+    a, b, kb, ka = synth.rotation_inputs(p, 3, 1, limbs=level)
+    want = ckks_np.conjugate(p, a, b, kb, ka)
+    ks = ckks.KeySet(p, None, None, conj=ckks.SwitchingKey(p.full_moduli, kb, a=ka))
+    ct = ckks.Ciphertext(RnsPoly(p.chain[:level], a, "eval"), RnsPoly(p.chain[:level], b, "eval"), 1.0)
+    out = ckks.conjugate(p, ks, ct)
+    assert np.array_equal(to_host(out.a.data), want[0]) and np.array_equal(to_host(out.b.data), want[1])
+
+
+def test_error_behaviour_matches_reference():
+    p = _params(12, 4, 1, 4)
+    a, b, kb, ka = synth.rotation_inputs(p, 1, 0)
+    ks = ckks.KeySet(p, None, None, rot={-1: ckks.SwitchingKey(p.full_moduli, kb, a=ka)})
+    ct = ckks.Ciphertext(RnsPoly(p.chain, a, "eval"), RnsPoly(p.chain, b, "eval"), 1.0)
+    with pytest.raises(KeyError):               # missing rotation key (ckks.py:664)
+        ckks.hrotate(p, ks, ct, (5,))
+    x = RnsPoly(p.chain, a, "eval")
+    y = RnsPoly(p.chain[:3], a[:3], "eval")
+    with pytest.raises(AssertionError):         # basis mismatch (rnspoly.py:174)
+        x.add(y)
+    with pytest.raises(AssertionError):         # rep mismatch
+        x.add(RnsPoly(p.chain, a, "coeff"))
+    with pytest.raises(AssertionError):         # mul needs eval rep (rnspoly.py:199)
+        RnsPoly(p.chain, a, "coeff").mul(RnsPoly(p.chain, a, "coeff"))
+    from paper_2112_06396_b200 import _lib
+    lib = _lib.load()
+    plan = plan_for(p)
+    assert lib.ck_rotate(plan.h, None, None, None, None, 0, 1, None, 0, None, None, None, 1, None) == -1
+    assert lib.ck_workspace_bytes(plan.h, 99, 1) == 0
+
+
+def test_plan_rejects_bad_modulus():
+    import ctypes as C
+    from paper_2112_06396_b200 import _lib
+    lib = _lib.load()
+    h = C.c_void_p()
+    ch = (C.c_uint64 * 1)(2 ** 40 + 1)            # not 1 mod 2N prime
+    assert lib.ck_plan_create(12, ch, 1, None, 0, 1, C.byref(h)) == -2
+    ch = (C.c_uint64 * 1)(prime_chain_below(1 << 12, 61, 1, 61, 0)[0][0])  # >= 2^60
+    assert lib.ck_plan_create(12, ch, 1, None, 0, 1, C.byref(h)) == -2
