@@ -149,6 +149,7 @@ struct ck_plan {
   int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
   int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
   int ks_intt_inline = 0;  // CKB200_KSINTT=1: special-row INTT row phase inside ks_row
+  int key_prefetch = 0;    // CKB200_KPF=1: bulk L2 prefetch of key tiles in ks_row (+4 GB DRAM re-reads, measured)
   int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   std::vector<u64> mod, psi;
@@ -578,6 +579,7 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ka_.intt_special = p->ks_intt_inline ? 1 : 0;
   ka_.dbg = p->ks_dbg;
   ka_.ws = p->ks_ws;
+  ka_.key_prefetch = p->key_prefetch;
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
@@ -650,6 +652,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     p->fused = !(e && e[0] == '1');
     const char* d = getenv("CKB200_KSDBG");
     p->ks_dbg = d ? atoi(d) : 0;
+    const char* kp = getenv("CKB200_KPF");
+    if (kp) p->key_prefetch = atoi(kp);
     const char* ki = getenv("CKB200_KSINTT");
     p->ks_intt_inline = ki ? atoi(ki) : 0;
     const char* wsv = getenv("CKB200_KSWS");

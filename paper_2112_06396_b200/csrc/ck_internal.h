@@ -49,6 +49,7 @@ struct KsRowArgs {
   int beta, l, R, logn, intt_special;
   int dbg;                      // timing experiments only (CKB200_KSDBG); 0 in production
   int ws;                       // warp-specialised persistent variant (CKB200_KSWS)
+  int key_prefetch;             // bulk L2 prefetch of the key tile at kernel start (CKB200_KPF)
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
 
