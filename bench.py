@@ -258,8 +258,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peak, peak_kind = _peaks()
     bytes_ks = ks_bytes(p)
     achieved = bytes_ks * B / (ms_step / 1000.0) / 1e9
+    traffic = args.traffic
+    if traffic is None:
+        try:  # committed ncu measurement (profiles/r01_traffic.json), per launch = per unit x B
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))[
+                "c3_dram_bytes_per_keyswitch"] * B
+        except Exception:
+            traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": args.traffic,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "profiles/r01_traffic.json (ncu dram bytes of one step, all launches)",
                 "kernel": "ck_rotate pipeline (batched key-switch, all launches of one step)",
                 "algorithmic_bytes_per_unit": bytes_ks, "units_per_launch": B,
                 "peak_kind": peak_kind}
@@ -420,7 +428,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per unit (from profiles/), reported as roofline.traffic")
+                    help="ncu dram bytes per launch (default: profiles/r01_traffic.json x units)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
