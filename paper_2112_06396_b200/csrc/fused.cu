@@ -101,8 +101,12 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsR
         u64 x[kE];
         row_from_smem<P2, 0, false>(x, g, srow);
         row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
+        // the 30-bit-split MAC only needs digits < 2^60: for q < 2^56 the lazy
+        // range [0, 16q) already is; larger (special) primes are reduced
+        if (q >= (1ull << 56)) {
 #pragma unroll
-        for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+          for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+        }
         __syncthreads();
         row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
       }
@@ -422,8 +426,13 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 8) md_row_kernel(MdRowArgs a
 #pragma unroll
   for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
   row_transform<P2, false, LOGN>(y, g, r << P2, srow, tw, q, two_q);
+  // conv stays lazy in [0, 16q) when x + 16q - conv fits 64 bits (q < 2^59);
+  // the Shoup multiply below accepts any 64-bit input
+  const bool lazy = q < (1ull << 59);
+  if (!lazy) {
 #pragma unroll
-  for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
+    for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
+  }
   __syncthreads();
   row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, srow);
   __syncthreads();
@@ -431,7 +440,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 8) md_row_kernel(MdRowArgs a
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
     const int c = sub_index<P2, 0, false>(g, k);
-    o[k] = shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
+    o[k] = lazy ? shoup(x[c] + (q << 4) - srow[sidx(c)], pinv.x, pinv.y, q)
+                : shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
   }
   if (a.addend && w) {
     const u64 t = a.galois ? a.galois[b] : a.galois_t;
