@@ -288,8 +288,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_e2e:
         from paper_2112_06396_b200.ckks import HostRotationPipeline
         ins = [wb.a, wb.b, wb.key_b, wb.key_a]
-        host_in = [t.cpu().pin_memory() for t in ins]
-        host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64).pin_memory() for _ in range(2)]
+        # pinned host buffers filled straight from the device (no pageable copy:
+        # at N=8 every rank holds ~10 GB of inputs)
+        host_in = []
+        for t in ins:
+            h = torch.empty(t.shape, dtype=torch.uint64, pin_memory=True)
+            h.copy_(t)
+            host_in.append(h)
+        host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
         del ins
         wb.release_inputs()  # the host pipeline owns its own device buffers
         pipe = HostRotationPipeline(p, B, chunk=args.e2e_chunk)
