@@ -236,4 +236,81 @@ CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
   }
 }
 
+// Row-phase pass with the CTA's row twiddles staged in shared memory.
+// Layout (tw_row_stage): stage s of the row phase (2^s twiddles per row)
+// occupies TR * 2^s entries at offset TR * (2^s - 1), row-major by local row.
+template <int P, int p, bool INV, int LOGN, int TR>
+CK_D void run_pass_rs(u64 (&x)[kE], int g, int rl, const ulonglong2* __restrict__ tws, u64 q,
+                      u64 two_q) {
+  constexpr int C = Sched<P>::C(p);
+  constexpr int LD = Sched<P>::logD(p, INV);
+  constexpr int NG = kE >> C;
+#pragma unroll
+  for (int h = 0; h < NG; ++h) {
+    const int s0 = sub_index<P, p, INV>(g, h << C);
+#pragma unroll
+    for (int st = 0; st < C; ++st) {
+      const int lhalf = INV ? st : (C - 1 - st);
+      const int half = 1 << lhalf;
+      const int logt = LD + lhalf;            // within-row distance
+      const int s = P - 1 - logt;             // row-phase stage: 2^s twiddles per row
+#pragma unroll
+      for (int b = 0; b < (1 << C) / (2 * half); ++b) {
+        const int k0 = b * 2 * half;
+        const int c = s0 + (k0 << LD);
+        const ulonglong2 w = tws[TR * ((1 << s) - 1) + (rl << s) + (c >> (logt + 1))];
+#pragma unroll
+        for (int k = k0; k < k0 + half; ++k) {
+          u64& X = x[(h << C) + k];
+          u64& Y = x[(h << C) + k + half];
+          if (INV) {
+            bfly_gs(X, Y, w.x, w.y, q, two_q);
+          } else {
+            const u64 t = shoup_lazy(Y, w.x, w.y, q);
+            const u64 xx = X;
+            X = xx + t;
+            Y = xx - t + two_q;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Stage the twiddles of rows [r0, r0+TR) of a 2^P-point row phase.
+template <int P, int P1, int TR, int NT>
+CK_D void tw_row_stage(ulonglong2* tws, const ulonglong2* __restrict__ tw, int r0) {
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const ulonglong2* src = tw + (1 << (P1 + s)) + ((long long)r0 << s);
+    for (int i = threadIdx.x; i < (TR << s); i += NT) tws[TR * ((1 << s) - 1) + i] = __ldg(src + i);
+  }
+}
+
+// Full row phase with staged twiddles (see row_transform).
+template <int P2, bool INV, int LOGN, int TR>
+CK_D void row_transform_rs(u64 (&x)[kE], int g, int rl, u64* srow, const ulonglong2* tws, u64 q,
+                           u64 two_q) {
+  constexpr int NP = Sched<P2>::np;
+  static_assert(NP <= 3, "row too long");
+  if (!INV) fwd_fold(x, q << 3);
+  run_pass_rs<P2, 0, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
+  if constexpr (NP > 1) {
+    __syncthreads();
+    row_to_smem<P2, 0, INV>(x, g, srow);
+    __syncthreads();
+    row_from_smem<P2, 1, INV>(x, g, srow);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass_rs<P2, 1, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
+  }
+  if constexpr (NP > 2) {
+    __syncthreads();
+    row_to_smem<P2, 1, INV>(x, g, srow);
+    __syncthreads();
+    row_from_smem<P2, 2, INV>(x, g, srow);
+    if (!INV) fwd_fold(x, q << 3);
+    run_pass_rs<P2, 2, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
+  }
+}
+
 }  // namespace ck
