@@ -120,6 +120,26 @@ int ck_rotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const u
               int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
               ck_stream stream);
 
+/* ---- hoisted rotations (ckks.hrotate, ckks.py:655-667) ----
+ * One shared ModUp of a; n_rot KSKIPs in one launch (shared evaluation-form
+ * digits, per-rotation key [n_rot][dnum][L+K][N] and Galois element, DEVICE
+ * uint64[n_rot]); ModDown pairs batched.  Outputs [n_rot][level][N] x 2.      */
+size_t ck_hrotate_workspace_bytes(const ck_plan* plan, int level, int n_rot);
+int ck_hrotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
+               const uint64_t* key_a, const uint64_t* galois, int level, int n_rot,
+               uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, ck_stream stream);
+
+/* ---- double-hoisted plaintext matrix-vector product (ckks.pt_matvec, ckks.py:684-719) ----
+ * diags: [n_rot + has_identity][level+K][N] raised-basis rows, rotated offsets
+ * first (matching key_b/key_a [n_rot][dnum][L+K][N]), identity last; galois:
+ * DEVICE uint64[n_rot + has_identity] (identity's element = 1).  One shared
+ * ModUp, batched KSKIP, diagonal MAC, one merged ModDown.  Output [level-1][N].  */
+size_t ck_pt_matvec_workspace_bytes(const ck_plan* plan, int level, int n_diag);
+int ck_pt_matvec(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
+                 const uint64_t* key_a, const uint64_t* galois, const uint64_t* diags, int level,
+                 int n_rot, int has_identity, uint64_t* out_a, uint64_t* out_b,
+                 uint64_t* workspace, ck_stream stream);
+
 /* ---- hoisted BSGS linear transform (composites.py:249-293) ----
  * == sum_{j=1..giant} rotate(pt_matvec(ct, {k: diag[j][k]}), -baby*j)  (ckks.py:684-719)
  * One shared ModUp; `baby` KSKIPs (Galois 5^k, k = 1..baby) in one launch;

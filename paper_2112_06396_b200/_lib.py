@@ -39,6 +39,11 @@ _SIGS = [
     ("ck_moddown", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_uint64, vp, C.c_int, vp]),
     ("ck_rotate", C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_uint64, vp, C.c_int, vp, vp, vp,
                             C.c_int, vp]),
+    ("ck_hrotate_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
+    ("ck_hrotate", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, vp]),
+    ("ck_pt_matvec_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
+    ("ck_pt_matvec", C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp,
+                               vp]),
     ("ck_bsgs_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int, C.c_int]),
     ("ck_bsgs", C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp,
                           vp, vp]),

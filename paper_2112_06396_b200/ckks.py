@@ -296,20 +296,31 @@ def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext,
 
 
 def hrotate(params: CkksParams, keys: KeySet, ct: Ciphertext, rotations) -> list[Ciphertext]:
-    """ckks.hrotate (ckks.py:655-667): one shared ModUp, per-rotation KSKIP+ModDown."""
+    """ckks.hrotate (ckks.py:655-667): one shared ModUp, all KSKIPs in one
+    launch, batched ModDown pairs -- a single ck_hrotate call."""
     limbs = ct.limbs
     assert ct.a.moduli == params.chain[:limbs]
-    dig = _decomp_modup_raw(params, ct.a.data, limbs)
-    outs = []
-    for r in rotations:
-        t = _galois(params, r)
-        key = keys.rot[r]  # KeyError like the reference (ckks.py:664)
-        u, v = _kskip_raw(params, dig, key, limbs, t)
-        a_out = _moddown_raw(params, u, limbs, 0)
-        b_out = _moddown_raw(params, v, limbs, 0, addend=ct.b.data, t=t)
-        mods = ct.a.moduli
-        outs.append(Ciphertext(RnsPoly(mods, a_out, "eval"), RnsPoly(mods, b_out, "eval"), ct.delta))
-    return outs
+    rotations = tuple(rotations)
+    if not rotations:
+        return []
+    keylist = [keys.rot[r] for r in rotations]  # KeyError like the reference (ckks.py:664)
+    plan = plan_for(params)
+    n = params.n_ring
+    kb = torch.stack([k.b for k in keylist]).contiguous()
+    ka = torch.stack([k.a for k in keylist]).contiguous()
+    gal = torch.tensor(np.array([_galois(params, r) for r in rotations], dtype=np.uint64),
+                       device="cuda")
+    nr = len(rotations)
+    out_a = torch.empty((nr, limbs, n), dtype=torch.uint64, device="cuda")
+    out_b = torch.empty_like(out_a)
+    nbytes = _L().ck_hrotate_workspace_bytes(plan.h, limbs, nr)
+    assert nbytes > 0
+    ws = torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
+    check(_L().ck_hrotate(plan.h, ptr(ct.a.data), ptr(ct.b.data), ptr(kb), ptr(ka), ptr(gal), limbs,
+                          nr, ptr(out_a), ptr(out_b), ptr(ws), stream_handle()), "ck_hrotate")
+    mods = ct.a.moduli
+    return [Ciphertext(RnsPoly(mods, out_a[i], "eval"), RnsPoly(mods, out_b[i], "eval"), ct.delta)
+            for i in range(nr)]
 
 
 def _rotate_raw(params, a, b, key: SwitchingKey, t: int, mode: int, limbs: int):
@@ -340,27 +351,39 @@ def conjugate(params: CkksParams, keys: KeySet, ct: Ciphertext) -> Ciphertext:
 
 def pt_matvec(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict,
               diag_delta: float) -> Ciphertext:
-    """ckks.pt_matvec (ckks.py:684-719), double-hoisted."""
+    """ckks.pt_matvec (ckks.py:684-719), double-hoisted, one ck_pt_matvec call:
+    shared ModUp, all KSKIPs in one launch, diagonal MAC on the raised basis,
+    one merged ModDown by P * q_last."""
     limbs = ct.limbs
     raised = params.raised_moduli(limbs)
-    dig = _decomp_modup_raw(params, ct.a.data, limbs)
-    acc_u = RnsPoly.zeros(raised, params.n_ring, "eval")
-    acc_v = RnsPoly.zeros(raised, params.n_ring, "eval")
-    for off, m_hat in sorted(diags.items()):
-        assert m_hat.moduli == raised
-        if off % params.slots == 0:
-            acc_u = acc_u.add(m_hat.mul(pmodup(params, ct.a)))
-            acc_v = acc_v.add(m_hat.mul(pmodup(params, ct.b)))
-            continue
-        r = -off
-        t = _galois(params, r)
-        u, v = _kskip_raw(params, dig, keys.rot[r], limbs, t)
-        b_hat = pmodup(params, ct.b.automorph(t))
-        acc_u = acc_u.add(m_hat.mul(RnsPoly(raised, u, "eval")))
-        acc_v = acc_v.add(m_hat.mul(RnsPoly(raised, v, "eval").add(b_hat)))
-    a_out = _moddown_merged(params, acc_u, limbs)
-    b_out = _moddown_merged(params, acc_v, limbs)
-    return Ciphertext(a_out, b_out, ct.delta * diag_delta / raised[limbs - 1])
+    n = params.n_ring
+    rot = [(off, m) for off, m in sorted(diags.items()) if off % params.slots != 0]
+    ident = [m for off, m in sorted(diags.items()) if off % params.slots == 0]
+    for _, m in list(rot) + [(0, m) for m in ident]:
+        assert m.moduli == raised
+    assert len(ident) <= 1
+    keylist = [keys.rot[-off] for off, _ in rot]
+    dev = dict(dtype=torch.uint64, device="cuda")
+    if keylist:
+        kb = torch.stack([k.b for k in keylist]).contiguous()
+        ka = torch.stack([k.a for k in keylist]).contiguous()
+    else:
+        kb = ka = None
+    gal = [_galois(params, -off) for off, _ in rot] + ([1] * len(ident))
+    galt = torch.tensor(np.array(gal, dtype=np.uint64), device="cuda")
+    dg = torch.stack([m.data for _, m in rot] + [m.data for m in ident]).contiguous()
+    out_a = torch.empty((limbs - 1, n), **dev)
+    out_b = torch.empty((limbs - 1, n), **dev)
+    plan = plan_for(params)
+    nbytes = _L().ck_pt_matvec_workspace_bytes(plan.h, limbs, len(gal))
+    assert nbytes > 0
+    ws = torch.empty(nbytes // 8, **dev)
+    check(_L().ck_pt_matvec(plan.h, ptr(ct.a.data), ptr(ct.b.data), ptr(kb), ptr(ka), ptr(galt),
+                            ptr(dg), limbs, len(rot), int(bool(ident)), ptr(out_a), ptr(out_b),
+                            ptr(ws), stream_handle()), "ck_pt_matvec")
+    mods = params.chain[:limbs - 1]
+    return Ciphertext(RnsPoly(mods, out_a, "eval"), RnsPoly(mods, out_b, "eval"),
+                      ct.delta * diag_delta / raised[limbs - 1])
 
 
 def bsgs(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict, diag_delta: float,

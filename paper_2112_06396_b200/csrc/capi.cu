@@ -973,6 +973,108 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
                 level, batch, st);
 }
 
+size_t ck_hrotate_workspace_bytes(const ck_plan* p, int level, int n_rot) {
+  if (!level_ok(p, level) || n_rot < 1 || p->K < 1) return 0;
+  const LevelTab& t = p->lv[level];
+  const long long rows = (long long)t.beta * t.R + level + (long long)n_rot * 2 * t.R +
+                         (long long)n_rot * 2 * level;
+  return (size_t)rows * p->n * sizeof(u64);
+}
+
+int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
+               const uint64_t* key_a_, const uint64_t* galois_, int level, int n_rot,
+               uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *kb = (const u64*)key_b_,
+            *ka = (const u64*)key_a_, *gal = (const u64*)galois_;
+  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
+  if (!level_ok(p, level) || !a || !b || !kb || !ka || !gal || !out_a || !out_b || !ws ||
+      n_rot < 1 || p->K < 1)
+    return CK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const LevelTab& t = p->lv[level];
+  const ModDownTab& m = t.md[0];
+  const long long N = p->n, l = level, R = t.R;
+  u64* dig = ws;
+  u64* tmp = dig + (long long)t.beta * R * N;
+  u64* uv = tmp + l * N;                          // [n][2][R][N]
+  u64* conv = uv + (long long)n_rot * 2 * R * N;  // [n][2][l][N]
+  // one shared ModUp (the hoisting, ckks.py:660), digits in evaluation form
+  CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
+  // every rotation's KSKIP in one launch: digits shared, automorphism folded
+  // into the gather, per-rotation key and Galois element
+  CK_TRY(kskip_impl(p, level, dig, kb, ka, 1, gal, uv, uv + R * N, 2 * R * N, n_rot, st, true));
+  // ModDown pair of every rotation (ckks.py:664-666): b is shared, gathered
+  // with each rotation's Galois element
+  CK_TRY(moddown_core(p, m, uv, R * N, conv, 2 * n_rot, st));
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, l * N, uv, 2 * R * N, conv, 2 * l * N, nullptr, 0,
+                m.d_keep_prime, m.d_pinv, 1, nullptr, level, n_rot, st));
+  return ew_run(p, ck::EW_MODDOWN, out_b, l * N, uv + R * N, 2 * R * N, conv + l * N, 2 * l * N, b,
+                0, m.d_keep_prime, m.d_pinv, 1, gal, level, n_rot, st);
+}
+
+size_t ck_pt_matvec_workspace_bytes(const ck_plan* p, int level, int n_diag) {
+  if (!level_ok(p, level) || level < 2 || n_diag < 1 || p->K < 1) return 0;
+  const LevelTab& t = p->lv[level];
+  const long long rows = (long long)t.beta * t.R + level + (long long)n_diag * 2 * t.R +
+                         2LL * t.R + 2LL * level;
+  return (size_t)rows * p->n * sizeof(u64);
+}
+
+int ck_pt_matvec(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
+                 const uint64_t* key_a_, const uint64_t* galois_, const uint64_t* diags_,
+                 int level, int n_rot, int has_identity, uint64_t* out_a_, uint64_t* out_b_,
+                 uint64_t* workspace_, ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *kb = (const u64*)key_b_,
+            *ka = (const u64*)key_a_, *gal = (const u64*)galois_, *diags = (const u64*)diags_;
+  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
+  const int nd = n_rot + (has_identity ? 1 : 0);
+  if (!level_ok(p, level) || level < 2 || !a || !b || !diags || !gal || !out_a || !out_b ||
+      !ws || n_rot < 0 || nd < 1 || nd > 32 || p->K < 1 || (n_rot > 0 && (!kb || !ka)))
+    return CK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const LevelTab& t = p->lv[level];
+  const ModDownTab& m = t.md[1];
+  const long long N = p->n, l = level, R = t.R, lo = l - 1;
+  u64* dig = ws;
+  u64* tmp = dig + (long long)t.beta * R * N;
+  u64* uvb = tmp + l * N;                      // [nd][2][R][N]
+  u64* acc = uvb + (long long)nd * 2 * R * N;  // [2][R][N]
+  u64* conv = acc + 2 * R * N;                 // [2][l][N]
+  if (n_rot > 0) {
+    CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
+    CK_TRY(kskip_impl(p, level, dig, kb, ka, 1, gal, uvb, uvb + R * N, 2 * R * N, n_rot, st, true));
+  }
+  if (has_identity) {
+    // identity diagonal (ckks.py:701-704): u = pmodup(a), v = 0 (+ P b added by
+    // the MAC kernel with Galois element 1 -> pmodup(b))
+    u64* ui = uvb + (long long)n_rot * 2 * R * N;
+    CK_TRY((int)cudaMemsetAsync(ui, 0, sizeof(u64) * 2 * R * N, st));
+    CK_TRY(ew_run(p, ck::EW_MULC, ui, 0, a, 0, nullptr, 0, nullptr, 0, t.d_chain_prime, t.d_pmod,
+                  1, nullptr, level, 1, st));
+  }
+  ck::DiagArgs da;
+  da.uv = uvb;
+  da.b = b;
+  da.diags = diags;
+  da.acc = acc;
+  da.galois = gal;  // [nd]: identity's element is 1 (set by the caller)
+  da.prime = t.d_raised_prime;
+  da.pmod = t.d_pmod;
+  da.pc = p->d_pc;
+  da.baby = nd;
+  da.giant = 1;
+  da.R = (int)R;
+  da.l = level;
+  da.logn = p->logn;
+  CK_TRY(ck::launch_diag_mac(da, st));
+  // one merged ModDown pair by P * q_last (ckks.py:712-717)
+  CK_TRY(moddown_core(p, m, acc, R * N, conv, 2, st));
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, 0, acc, 0, conv, 0, nullptr, 0, m.d_keep_prime, m.d_pinv,
+                1, nullptr, (int)lo, 1, st));
+  return ew_run(p, ck::EW_MODDOWN, out_b, 0, acc + R * N, 0, conv + lo * N, 0, nullptr, 0,
+                m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, 1, st);
+}
+
 size_t ck_bsgs_workspace_bytes(const ck_plan* p, int level, int baby, int giant) {
   if (!level_ok(p, level) || level < 2 || baby < 1 || giant < 1) return 0;
   const LevelTab& t = p->lv[level];

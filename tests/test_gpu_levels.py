@@ -11,6 +11,7 @@ import pytest
 import torch
 
 import cases
+import gpu_backend
 from oracle import ckks_np
 from paper_2112_06396_b200 import ckks, synth
 from paper_2112_06396_b200.device import plan_for, to_dev, to_host
@@ -99,3 +100,18 @@ def test_plan_rejects_bad_modulus():
     assert lib.ck_plan_create(12, ch, 1, None, 0, 1, C.byref(h)) == -2
     ch = (C.c_uint64 * 1)(prime_chain_below(1 << 12, 61, 1, 61, 0)[0][0])  # >= 2^60
     assert lib.ck_plan_create(12, ch, 1, None, 0, 1, C.byref(h)) == -2
+
+
+@pytest.mark.parametrize("offs", [(0,), (2, 6), (0, 1, 2, 3, 4, 5, 6, 7, 9, 11), (-3, 4)])
+def test_pt_matvec_diagonal_sets(offs):
+    """ck_pt_matvec: identity-only, rotations-only, many diagonals, negative offsets."""
+    p = cases.make_params(cases.TOY_A)
+    mods, raised = p.chain, p.raised_moduli(p.limbs)
+    a = cases._rows(p, 0, synth.TAG_CT_A, mods)
+    b = cases._rows(p, 0, synth.TAG_CT_B, mods)
+    diags = {o: cases._rows(p, 0, synth.TAG_DIAG, raised, digit=o % 64) for o in offs}
+    keys = cases._keys(p, [-o for o in offs if o % p.slots])
+    want = cases.OracleBackend().pt_matvec(p, a, b, keys, diags)
+    got = gpu_backend.GpuBackend().pt_matvec(p, a, b, keys, diags)
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
