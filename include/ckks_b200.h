@@ -155,6 +155,20 @@ int ck_bsgs(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uin
             int level, int baby, int giant, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace,
             ck_stream stream);
 
+/* ---- compressed evaluation keys: SHAKE256 uniform rows (ckks.py:169-215) ----
+ * ck_xof_uniform: row r = first n words of SHAKE256(msgs[r][0:msg_lens[r]])
+ * (little-endian u64) below floor(2^64/q_r)*q_r, each reduced mod q_r
+ * (ckks._xof_uniform, ckks.py:169-185).  msgs, msg_lens, moduli: DEVICE arrays.
+ * ck_expand_key_a: the a-rows of n_keys compressed switching keys
+ * (SwitchingKey.expand, ckks.py:207-215): key_a[k][j][i] =
+ * _xof_uniform(seed_k || "ksk<j>:<i>", q_i, N) over the plan's full basis
+ * (chain || special) and its top-level digit count; seeds [n_keys][seed_stride]
+ * and seed_lens [n_keys] are DEVICE arrays; output [n_keys][dnum][L+K][N].  */
+int ck_xof_uniform(const uint8_t* msgs, const int32_t* msg_lens, int64_t msg_stride,
+                   const uint64_t* moduli, int rows, int n, uint64_t* out, ck_stream stream);
+int ck_expand_key_a(const ck_plan* plan, const uint8_t* seeds, const int32_t* seed_lens,
+                    int64_t seed_stride, int n_keys, uint64_t* key_a, ck_stream stream);
+
 /* ---- synthetic inputs: counter-based uniform residues (paper_2112_06396_b200.synth) ----
  * row r: out[r][k] = mulhi(splitmix64(keys[r] + k), qs[r]).  keys, qs: DEVICE. */
 int ck_fill_uniform(uint64_t* out, int64_t rows, int log_n, const uint64_t* keys,

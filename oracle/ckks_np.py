@@ -476,3 +476,34 @@ def bsgs(params, a, b, keys: dict, diags: dict, baby: int, giant: int):
         else:
             out_a, out_b = addmod(out_a, ra, ql), addmod(out_b, rb, ql)
     return out_a, out_b
+
+
+# ------------------------------------------------------------------ compressed keys
+
+def xof_uniform(seed: bytes, tag: bytes, q: int, n: int) -> np.ndarray:
+    """ckks._xof_uniform (ckks.py:169-185): the first n little-endian u64
+    words of SHAKE256(seed || tag) that are < floor(2^64/q)*q, each mod q.
+    (The reference squeezes in chunks via digest(offset + length)[offset:];
+    the chunks are consecutive slices of one stream, so one long squeeze with
+    the same rejection rule is the same sequence.)"""
+    import hashlib
+    bound = (1 << 64) // q * q
+    out = np.empty(n, dtype=np.uint64)
+    have, length = 0, 8 * (n + n // 8 + 16)
+    while True:
+        raw = np.frombuffer(hashlib.shake_256(seed + tag).digest(length), dtype="<u8")
+        keep = raw[raw < np.uint64(bound)] if bound < (1 << 64) else raw
+        if keep.size >= n:
+            out[:] = keep[:n] % np.uint64(q)
+            return out
+        length *= 2
+
+
+def expand_key_a(seed: bytes, moduli, digits: int, n: int) -> np.ndarray:
+    """SwitchingKey.expand (ckks.py:207-215): a[j][i] = xof_uniform(seed,
+    b"ksk%d:%d" % (j, i), moduli[i], n) over the full basis."""
+    a = np.empty((digits, len(moduli), n), dtype=np.uint64)
+    for j in range(digits):
+        for i, q in enumerate(moduli):
+            a[j, i] = xof_uniform(seed, b"ksk%d:%d" % (j, i), q, n)
+    return a

@@ -41,6 +41,8 @@ _SIGS = [
                             C.c_int, vp]),
     ("ck_hrotate_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
     ("ck_hrotate", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, vp]),
+    ("ck_xof_uniform", C.c_int, [vp, vp, C.c_int64, vp, C.c_int, C.c_int, vp, vp]),
+    ("ck_expand_key_a", C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, vp]),
     ("ck_pt_matvec_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
     ("ck_pt_matvec", C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp,
                                vp]),
@@ -74,6 +76,9 @@ def load(path: str = LIB_PATH):
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+CK_ERR_ARG, CK_ERR_MODULUS, CK_ERR_ALLOC, CK_ERR_DEVICE = -1, -2, -3, -4
 
 
 def check(rc: int, what: str = "") -> None:

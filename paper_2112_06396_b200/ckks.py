@@ -37,8 +37,8 @@ class SwitchingKey:
     """ckks.SwitchingKey (ckks.py:188-225); expanded keys only on the device.
 
     b, a: (dnum, L+K, N) full-basis rows.  A compressed key (seed, a=None) is
-    expanded on the host with the reference's SHAKE256 XOF before upload
-    (on-device expansion is the next item in SURVEY 8(f)).
+    expanded on the device with the reference's SHAKE256 XOF (ck_expand_key_a);
+    only b and the seed cross the host boundary.
     """
 
     moduli: tuple[int, ...]
@@ -50,7 +50,7 @@ class SwitchingKey:
         self.b = to_dev(self.b)
         if self.a is None:
             assert self.seed is not None
-            self.a = to_dev(_expand_a(self.seed, self.moduli, tuple(self.b.shape)))
+            self.a = _expand_one(self.seed, self.moduli, tuple(self.b.shape))
         else:
             self.a = to_dev(self.a)
 
@@ -59,33 +59,53 @@ class SwitchingKey:
         return False
 
 
-def _xof_uniform(seed: bytes, label: bytes, q: int, n: int) -> np.ndarray:
-    """Restatement of ckks._xof_uniform (ckks.py:169-185): SHAKE256 stream,
-    rejection of words >= floor(2^64/q)*q, then % q; host-side key expansion."""
-    import hashlib
-    bound = np.uint64((1 << 64) // q * q)
-    out = np.empty(n, dtype=np.uint64)
-    have, offset = 0, 0
-    length = 8 * (n + n // 8 + 16)
-    xof = hashlib.shake_256(seed + label)
-    while have < n:
-        raw = np.frombuffer(xof.digest(offset + length)[offset:], dtype="<u8")
-        offset += length
-        keep = raw[raw < bound]
-        take = min(n - have, keep.size)
-        out[have:have + take] = keep[:take] % np.uint64(q)
-        have += take
-        length = 8 * (n - have + 16)
+def _expand_one(seed: bytes, moduli, shape) -> torch.Tensor:
+    """SwitchingKey.expand (ckks.py:207-215) of one key: every (digit, limb)
+    row is one ck_xof_uniform stream over seed || b"ksk<digit>:<limb>"."""
+    dn, lm, n = shape
+    msgs = [seed + b"ksk%d:%d" % (j, i) for j in range(dn) for i in range(lm)]
+    msg, lens, stride = _seed_tensor(msgs)
+    mods = torch.tensor(np.array([moduli[i] for _ in range(dn) for i in range(lm)],
+                                 dtype=np.uint64), device="cuda")
+    out = torch.empty(shape, dtype=torch.uint64, device="cuda")
+    check(_L().ck_xof_uniform(ptr(msg), ptr(lens), stride, ptr(mods), dn * lm, n, ptr(out),
+                              stream_handle()), "ck_xof_uniform")
     return out
 
 
-def _expand_a(seed: bytes, moduli, shape) -> np.ndarray:
-    dn, lm, n = shape
-    a = np.empty(shape, dtype=np.uint64)
-    for j in range(dn):
-        for i in range(lm):
-            a[j, i] = _xof_uniform(seed, b"ksk%d:%d" % (j, i), moduli[i], n)
-    return a
+def _seed_tensor(seeds: list[bytes]):
+    stride = max(1, max(len(x) for x in seeds))
+    buf = np.zeros((len(seeds), stride), dtype=np.uint8)
+    for k, x in enumerate(seeds):
+        buf[k, :len(x)] = np.frombuffer(x, dtype=np.uint8)
+    lens = np.array([len(x) for x in seeds], dtype=np.int32)
+    return torch.from_numpy(buf).cuda(), torch.from_numpy(lens).cuda(), stride
+
+
+def _xof_uniform(seed: bytes, tag: bytes, q: int, n: int) -> torch.Tensor:
+    """ckks._xof_uniform (ckks.py:169-185) on the device (ck_xof_uniform):
+    n words of SHAKE256(seed || tag) below floor(2^64/q)*q, reduced mod q."""
+    msg, lens, stride = _seed_tensor([seed + tag])
+    mods = torch.tensor(np.array([q], dtype=np.uint64), device="cuda")
+    out = torch.empty((1, n), dtype=torch.uint64, device="cuda")
+    check(_L().ck_xof_uniform(ptr(msg), ptr(lens), stride, ptr(mods), 1, n, ptr(out),
+                              stream_handle()), "ck_xof_uniform")
+    return out[0]
+
+
+def expand_key_a(params: CkksParams, seeds: list[bytes], out: torch.Tensor | None = None):
+    """SwitchingKey.expand (ckks.py:207-215) for a batch of compressed keys on
+    the device (ck_expand_key_a): out[k][j][i] = _xof_uniform(seeds[k],
+    b"ksk%d:%d" % (j, i), full_moduli[i], N).  Returns (n_keys, dnum, L+K, N)."""
+    dn = len(params.digit_spans(params.limbs))
+    shape = (len(seeds), dn, len(params.full_moduli), params.n_ring)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.uint64, device="cuda")
+    assert tuple(out.shape) == shape and out.is_contiguous()
+    msg, lens, stride = _seed_tensor(seeds)
+    check(_L().ck_expand_key_a(plan_for(params).h, ptr(msg), ptr(lens), stride, len(seeds),
+                               ptr(out), stream_handle()), "ck_expand_key_a")
+    return out
 
 
 @dataclass

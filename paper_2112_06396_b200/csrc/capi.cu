@@ -154,6 +154,7 @@ struct ck_plan {
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
+  u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
   ulonglong2* d_tw = nullptr;
   ulonglong2* d_itw = nullptr;
   Tw4* d_ctw = nullptr;   // column-phase twiddles, FP64-assisted form [prime][2^P1]
@@ -707,6 +708,7 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   }
   int err = 0;
   p->d_pc = upload(p->allocs, pcs, &err);
+  p->d_mod = upload(p->allocs, p->mod, &err);
   p->d_tw = upload(p->allocs, tw, &err);
   p->d_itw = upload(p->allocs, itw, &err);
   if (log_n >= 12) {  // split transforms: column phase of 2^P1 points
@@ -1162,6 +1164,47 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint
                   1, nullptr, (int)lo, 1, st));
   }
   return 0;
+}
+
+int ck_xof_uniform(const uint8_t* msgs, const int32_t* msg_lens, int64_t msg_stride,
+                    const uint64_t* moduli, int rows, int n, uint64_t* out, ck_stream stream) {
+  if (rows < 0 || n < 0 || (rows > 0 && (!msgs || !msg_lens || !moduli || !out)) ||
+      msg_stride < 0)
+    return CK_ERR_ARG;
+  if (rows == 0 || n == 0) return 0;
+  ck::XofArgs a;
+  a.msg = msgs;
+  a.msg_len = msg_lens;
+  a.msg_stride = msg_stride;
+  a.moduli = (const u64*)moduli;
+  a.out = (u64*)out;
+  a.rows = rows;
+  a.rows_per_item = 1;
+  a.limbs = 1;
+  a.n = n;
+  a.tag_mode = 0;
+  return ck::launch_xof(a, (cudaStream_t)stream);
+}
+
+int ck_expand_key_a(const ck_plan* p, const uint8_t* seeds, const int32_t* seed_lens,
+                    int64_t seed_stride, int n_keys, uint64_t* key_a, ck_stream stream) {
+  if (!p || n_keys < 0 || seed_stride < 0 || (n_keys > 0 && (!seeds || !seed_lens || !key_a)))
+    return CK_ERR_ARG;
+  if (n_keys == 0) return 0;
+  const int limbs = p->L + p->K;
+  const int digits = p->lv[p->L].beta;
+  ck::XofArgs a;
+  a.msg = seeds;
+  a.msg_len = seed_lens;
+  a.msg_stride = seed_stride;
+  a.moduli = p->d_mod;
+  a.out = (u64*)key_a;
+  a.rows_per_item = digits * limbs;
+  a.rows = n_keys * a.rows_per_item;
+  a.limbs = limbs;
+  a.n = p->n;
+  a.tag_mode = 1;
+  return ck::launch_xof(a, (cudaStream_t)stream);
 }
 
 int ck_fill_uniform(uint64_t* out_, int64_t rows, int log_n, const uint64_t* keys_,

@@ -152,6 +152,18 @@ struct EwArgs {
 };
 int launch_ew(const EwArgs& a, int rows, int batch, cudaStream_t st);
 
+// SHAKE256 uniform rows (xof.cu)
+struct XofArgs {
+  const unsigned char* msg;     // [items][msg_stride] seed bytes (device)
+  const int* msg_len;           // [items] (device)
+  long long msg_stride;
+  const u64* moduli;            // tag_mode: [limbs] per limb; else [rows]
+  u64* out;                     // [rows][n]
+  int rows, rows_per_item, limbs, n;
+  int tag_mode;                 // 1: message = seed || "ksk<digit>:<limb>" (row = digit*limbs+limb)
+};
+int launch_xof(const XofArgs& a, cudaStream_t st);
+
 int launch_fill_uniform(u64* out, long long rows, int logn, const u64* keys, const u64* qs,
                         cudaStream_t st);
 
