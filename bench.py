@@ -298,7 +298,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
         del ins
         wb.release_inputs()  # the host pipeline owns its own device buffers
-        pipe = HostRotationPipeline(p, B, chunk=args.e2e_chunk)
+        pipe = HostRotationPipeline(p, B, chunk=args.e2e_chunk, nbuf=args.e2e_nbuf)
         ke = max(1, min(args.steps, args.e2e_steps))
         pipe.run(*host_in, wb.galois, *host_out)  # warm-up
         torch.cuda.synchronize()
@@ -316,10 +316,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "d2h_bytes_per_step": sum(t.numel() * 8 for t in host_out),
                "steps": ke,
                "note": ("ciphertexts AND per-rotation evaluation keys copied H2D every step "
-                        f"(HostRotationPipeline, chunks of {args.e2e_chunk} overlap PCIe with compute)")}
+                        f"(HostRotationPipeline, chunks of {args.e2e_chunk}, {args.e2e_nbuf} buffers, overlap PCIe with compute)")}
         # bit-exact: host outputs equal the device-resident outputs
         e2e["matches_device_outputs"] = bool(
             torch.equal(host_out[0], wb.out_a.cpu()) and torch.equal(host_out[1], wb.out_b.cpu()))
+        if not args.no_compressed:
+            e2e["compressed_keys"] = e2e_compressed(args, p, B, world, wb, host_in, host_out, pipe,
+                                                    stream, max_over_ranks, barrier, units)
 
     # ---- CPU baseline (oracle port on host cores), rank 0 at N=1
     cpu = None
@@ -352,6 +355,50 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.destroy_process_group()
 
+
+
+def e2e_compressed(args, p, B, world, wb, host_in, host_out, pipe, stream, max_over_ranks,
+                   barrier, units):
+    """End to end with COMPRESSED rotation keys (the reference's keygen default,
+    ckkslab ckks.py:310-312): per unit the host holds (a, b, key b-rows, key
+    seed); only those cross PCIe and the key a-rows are expanded on the device
+    with SHAKE256 (ck_expand_key_a) inside the timed region.  Same key-switch
+    count and shapes as the headline e2e; the key a-rows are different values
+    (XOF output instead of the counter generator), so parity is checked against
+    a device-resident rotate_batch of the same compressed keys."""
+    import torch
+    from paper_2112_06396_b200 import ckks
+    seed_root = int(p.seed).to_bytes(8, "little")
+    two_n = 2 * p.n_ring
+    seeds = [b"rot%d" % ((-k) % two_n) + seed_root for k in wb.ks]
+    a_h, b_h, kb_h = host_in[0], host_in[1], host_in[2]
+    ke = max(1, min(args.steps, args.e2e_steps))
+    pipe.run(a_h, b_h, kb_h, None, wb.galois, *host_out, key_seeds=seeds)  # warm-up
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        pipe.run(a_h, b_h, kb_h, None, wb.galois, *host_out, key_seeds=seeds)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = max_over_ranks(e0.elapsed_time(e1))
+    seed_bytes = sum(len(x) for x in seeds) + 4 * len(seeds)
+    out = {"value": B * world * ke / (ems / 1000.0), "unit": UNIT,
+           "h2d_bytes_per_step": sum(t.numel() * 8 for t in (a_h, b_h, kb_h)) + seed_bytes,
+           "d2h_bytes_per_step": sum(t.numel() * 8 for t in host_out), "steps": ke,
+           "note": "key b-rows + seeds over PCIe; a-rows SHAKE256-expanded on device in the timed region"}
+    # parity: first 4 units through the device-resident path with the same keys
+    m = min(4, B)
+    ka = ckks.expand_key_a(p, seeds[:m])
+    dev = [t[:m].cuda() for t in (a_h, b_h, kb_h)]
+    oa, ob = torch.empty_like(dev[0]), torch.empty_like(dev[1])
+    ckks.rotate_batch(p, dev[0], dev[1], dev[2], ka, wb.galois[:m], oa, ob)
+    torch.cuda.synchronize()
+    out["matches_device_outputs"] = bool(torch.equal(oa.cpu(), host_out[0][:m]) and
+                                         torch.equal(ob.cpu(), host_out[1][:m]))
+    return out
 
 def run_config(args, rank: int, world: int, local_rank: int):
     """Non-default BASELINE configs (C1, C2, C4, C5): device-resident throughput only."""
@@ -431,7 +478,10 @@ def main():
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=8)
+    ap.add_argument("--e2e-nbuf", type=int, default=4, help="device chunk buffers in the host pipeline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-compressed", action="store_true",
+                    help="skip the compressed-key variant of the end-to-end measurement")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch (default: profiles/r01_traffic.json x units)")

@@ -73,6 +73,17 @@ def _expand_one(seed: bytes, moduli, shape) -> torch.Tensor:
     return out
 
 
+def _seed_tensor_host(seeds: list[bytes]):
+    """Pinned (seed bytes [n][stride], lengths [n]) for an async upload."""
+    stride = max(1, max(len(x) for x in seeds))
+    buf = torch.zeros((len(seeds), stride), dtype=torch.uint8, pin_memory=True)
+    for k, x in enumerate(seeds):
+        if x:
+            buf[k, :len(x)] = torch.frombuffer(bytearray(x), dtype=torch.uint8)
+    lens = torch.tensor([len(x) for x in seeds], dtype=torch.int32).pin_memory()
+    return buf, lens, stride
+
+
 def _seed_tensor(seeds: list[bytes]):
     stride = max(1, max(len(x) for x in seeds))
     buf = np.zeros((len(seeds), stride), dtype=np.uint8)
@@ -501,9 +512,15 @@ class HostRotationPipeline:
     The batch is cut into chunks; chunk c+1's host->device copy and chunk c-1's
     device->host copy run on their own streams while chunk c computes, so the
     PCIe transfers (8 GB of keys per 64 C3 rotations) overlap the key-switch.
+
+    Compressed keys (the reference's keygen default for rotation keys,
+    ckks.py:310-312): pass ``key_a=None`` and ``key_seeds`` (a list of seed
+    bytes, one per unit).  Only b-rows and seeds cross PCIe; all a-rows are
+    expanded on the device (ck_expand_key_a) on a fourth stream while the
+    first chunks are still in flight, halving the key bytes on the bus.
     """
 
-    def __init__(self, params: CkksParams, batch: int, chunk: int = 8):
+    def __init__(self, params: CkksParams, batch: int, chunk: int = 8, nbuf: int = 4):
         self.params = params
         self.plan = plan_for(params)
         self.batch, self.chunk = batch, min(chunk, batch)
@@ -515,36 +532,64 @@ class HostRotationPipeline:
         self.buf = [dict(a=torch.empty((C, L, n), **dev), b=torch.empty((C, L, n), **dev),
                          kb=torch.empty((C, dn, full, n), **dev), ka=torch.empty((C, dn, full, n), **dev),
                          oa=torch.empty((C, L, n), **dev), ob=torch.empty((C, L, n), **dev))
-                    for _ in range(2)]
+                    for _ in range(max(2, min(nbuf, -(-batch // self.chunk))))]
         self.ws = self.plan.workspace(L, C, "hostpipe")
         self.s_h2d = torch.cuda.Stream()
         self.s_d2h = torch.cuda.Stream()
         self.s_comp = torch.cuda.Stream()
+        self.s_xof = torch.cuda.Stream()
+        self.ka_all = None
+        self._seed_cache = None
 
-    def run(self, a, b, key_b, key_a, galois, out_a, out_b) -> None:
+    def _seeds(self, key_seeds):
+        if self._seed_cache is None or self._seed_cache[0] is not key_seeds:
+            self._seed_cache = (key_seeds, _seed_tensor_host(key_seeds))
+        return self._seed_cache[1]
+
+    def run(self, a, b, key_b, key_a, galois, out_a, out_b, key_seeds=None) -> None:
         """a, b, key_b, key_a, out_a, out_b: pinned host tensors ([B][...]);
-        galois: (B,) uint64 DEVICE tensor.  Stream-ordered after the current stream."""
+        galois: (B,) uint64 DEVICE tensor.  Stream-ordered after the current stream.
+        key_a=None with key_seeds: compressed keys, a-rows expanded on the device."""
         cur = torch.cuda.current_stream()
         start = torch.cuda.Event()
         start.record(cur)
-        for s in (self.s_h2d, self.s_d2h, self.s_comp):
+        for s in (self.s_h2d, self.s_d2h, self.s_comp, self.s_xof):
             s.wait_event(start)
-        loaded = [torch.cuda.Event() for _ in range(2)]
-        computed = [torch.cuda.Event() for _ in range(2)]
-        freed = [None, None]
+        compressed = key_a is None
+        if compressed:
+            assert key_seeds is not None and len(key_seeds) == self.batch
+            p = self.params
+            shape = (self.batch, len(p.digit_spans(p.limbs)), len(p.full_moduli), p.n_ring)
+            if self.ka_all is None:
+                self.ka_all = torch.empty(shape, dtype=torch.uint64, device="cuda")
+            hmsg, hlens, stride = self._seeds(key_seeds)
+            expanded = torch.cuda.Event()
+            with torch.cuda.stream(self.s_xof):
+                msg = hmsg.to("cuda", non_blocking=True)
+                lens = hlens.to("cuda", non_blocking=True)
+                check(_L().ck_expand_key_a(self.plan.h, ptr(msg), ptr(lens), stride, self.batch,
+                                           ptr(self.ka_all), stream_handle()), "ck_expand_key_a")
+                expanded.record(self.s_xof)
+            self.s_comp.wait_event(expanded)
+        nb = len(self.buf)
+        loaded = [torch.cuda.Event() for _ in range(nb)]
+        computed = [torch.cuda.Event() for _ in range(nb)]
+        freed = [None] * nb
         for ci, c0 in enumerate(range(0, self.batch, self.chunk)):
-            s = ci % 2
+            s = ci % nb
             cc = min(self.chunk, self.batch - c0)
             bf = self.buf[s]
             with torch.cuda.stream(self.s_h2d):
                 if freed[s] is not None:
                     self.s_h2d.wait_event(freed[s])
-                for name, src in (("a", a), ("b", b), ("kb", key_b), ("ka", key_a)):
+                srcs = (("a", a), ("b", b), ("kb", key_b)) + (() if compressed else (("ka", key_a),))
+                for name, src in srcs:
                     bf[name][:cc].copy_(src[c0:c0 + cc], non_blocking=True)
                 loaded[s].record(self.s_h2d)
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(loaded[s])
-                rotate_batch(self.params, bf["a"][:cc], bf["b"][:cc], bf["kb"][:cc], bf["ka"][:cc],
+                ka = self.ka_all[c0:c0 + cc] if compressed else bf["ka"][:cc]
+                rotate_batch(self.params, bf["a"][:cc], bf["b"][:cc], bf["kb"][:cc], ka,
                              galois[c0:c0 + cc], bf["oa"][:cc], bf["ob"][:cc], self.ws)
                 computed[s].record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):
@@ -554,5 +599,5 @@ class HostRotationPipeline:
                 ev = torch.cuda.Event()
                 ev.record(self.s_d2h)
                 freed[s] = ev
-        for s in (self.s_h2d, self.s_d2h, self.s_comp):
+        for s in (self.s_h2d, self.s_d2h, self.s_comp, self.s_xof):
             cur.wait_stream(s)

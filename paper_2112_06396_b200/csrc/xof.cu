@@ -61,7 +61,7 @@ __device__ __forceinline__ u64 reduce_word(u64 w, u64 q, u64 m) {
 
 constexpr int kRate = 136;
 constexpr int kRateWords = 17;
-constexpr int kThreads = 64;
+constexpr int kThreads = 32;  // spread the latency-bound row streams over more SMs
 
 __global__ void __launch_bounds__(kThreads) xof_kernel(XofArgs a) {
   __shared__ u64 stage[kThreads][kRateWords];
