@@ -139,6 +139,173 @@ static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
   bconv_kernel<NS><<<grid, kBcThreads, smem, st>>>(G);
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core form.  The contraction is exact integer arithmetic, so it can
+// run on the INT8 tensor cores (mma.sync m16n8k32 u8.u8.s32; measured
+// 568 T MAC/s on this B200, profiles/r01_mma_microbench.txt) instead of the
+// IMAD pipe that bounds the rest of the key-switch:
+//   x_i        = sum_a x_ia 2^{8a}                 (little-endian bytes, a < 8)
+//   T'_{iaj}   = T_ij 2^{8a} mod p_j = sum_b T'_{iajb} 2^{8b}
+//   S_jb       = sum_{i,a} x_ia T'_{iajb}          (< 64 * 255^2 < 2^22 per 32-byte k-step pair)
+//   y_j       == sum_b S_jb 2^{8b}   (mod p_j)
+// A = [coefficients][(i,a)] is the byte view of the u64 source rows (no
+// repacking: a 32-bit A-fragment register is one half of one u64), B =
+// [(i,a)][(j,b)] is precomputed per plan in fragment order.  The n-tiles are
+// arranged so that lane (gid, tig) ends up holding all eight S_jb of target
+// j = 4g + tig for rows gid and gid + 8; the epilogue per (coefficient,
+// target) is two 32x64-bit Shoup products instead of 8 sources x 4 IMAD.WIDE
+// plus a 128-bit reduction.
+constexpr int kTcWarps = 4;
+constexpr int kTcRows = kTcWarps * 32;  // coefficients per CTA (2 m16 blocks per warp)
+constexpr int kTcXs = kTcRows + 8;      // padded u64 row stride of the staged sources
+
+__device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+// x * w mod p in [0, 2p) for x < 2^32 (Shoup, wp = floor(w 2^64 / p))
+__device__ __forceinline__ u64 shoup_lazy32(u32 x, u64 w, u64 wp, u64 p) {
+  const u64 t = (u64)x * (u32)wp;
+  const u64 u = (u64)x * (u32)(wp >> 32) + (t >> 32);
+  const u32 qh = (u32)(u >> 32);
+  return (u64)x * w - (u64)qh * p;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kTcWarps * 32, 4) bconv_tc_kernel(const __grid_constant__ BconvGroups G) {
+  const BconvArgs& a = G.g[blockIdx.y];
+  extern __shared__ __align__(16) unsigned char tc_smem[];
+  const int nd = a.nd, ns = a.ns;
+  const int ngrp = (nd + 3) >> 2;
+  const int ntile = ngrp * 4;
+  const int tks = a.tc_ks;
+  u64* xs = (u64*)tc_smem;                                  // [4*KS][kTcXs]
+  uint2* bf = (uint2*)(xs + 4 * KS * kTcXs);                // [tks][ntile][32]
+  ulonglong2* cs = (ulonglong2*)(bf + tks * ntile * 32);    // [nd][2]
+  u64* ps = (u64*)(cs + 2 * nd);                            // [nd]
+  u64* kQs = ps + nd;                                       // [nd][ns+1] (centered)
+  unsigned char* kk = (unsigned char*)(kQs + (a.centered ? nd * (ns + 1) : 0));  // [kTcRows]
+  const int tid = threadIdx.x;
+  for (int i = tid; i < tks * ntile * 32; i += blockDim.x) bf[i] = a.Bf[i];
+  for (int j = tid; j < nd; j += blockDim.x) {
+    cs[2 * j] = a.c3248[2 * j];
+    cs[2 * j + 1] = a.c3248[2 * j + 1];
+    ps[j] = a.pc[a.dst_prime[j]].q;
+  }
+  if (a.centered)
+    for (int i = tid; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
+
+  const int n = 1 << a.logn;
+  const int row0 = blockIdx.x * kTcRows;
+  const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
+  for (int e = tid; e < 4 * KS * kTcRows; e += blockDim.x) {
+    const int i = e / kTcRows, r = e - i * kTcRows;
+    u64 v = 0;
+    if (i < ns && row0 + r < n) {
+      const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
+      v = in[off + row0 + r];
+      if (a.src_scale) {
+        const ulonglong2 sc = a.src_scale[i];
+        v = shoup(v, sc.x, sc.y, a.pc[a.src_prime[i]].q);
+      }
+    }
+    xs[i * kTcXs + r] = v;
+  }
+  __syncthreads();
+  if (a.centered) {
+    // k = rint(sum_i fl(v_i) w_i) in the reference's op order (rnspoly.py:320-325)
+    for (int r = tid; r < kTcRows; r += blockDim.x) {
+      double est = 0.0;
+      for (int i = 0; i < ns; ++i)
+        est = __dadd_rn(est, __dmul_rn(__ull2double_rn(xs[i * kTcXs + r]), a.w[i]));
+      kk[r] = (unsigned char)rint(est);
+    }
+    __syncthreads();
+  }
+
+  const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
+  const u32* xw = (const u32*)xs;
+  u32 af[2][KS][4];
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int r = warp * 32 + mb * 16 + gid;
+      const int i0 = 4 * s + (tig >> 1), i1 = i0 + 2, w = tig & 1;
+      af[mb][s][0] = xw[(i0 * kTcXs + r) * 2 + w];
+      af[mb][s][1] = xw[(i0 * kTcXs + r + 8) * 2 + w];
+      af[mb][s][2] = xw[(i1 * kTcXs + r) * 2 + w];
+      af[mb][s][3] = xw[(i1 * kTcXs + r + 8) * 2 + w];
+    }
+  u64* out = a.out + (long long)blockIdx.z * a.out_batch;
+  for (int g = 0; g < ngrp; ++g) {
+    int acc[2][4][4];
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[mb][u][c] = 0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      if (s < tks) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint2 b = bf[(s * ntile + g * 4 + u) * 32 + lane];
+          mma_u8(acc[0][u], af[0][s], b);
+          mma_u8(acc[1][u], af[1][s], b);
+        }
+      }
+    }
+    const int j = g * 4 + tig;
+    if (j < nd) {
+      const u64 p = ps[j];
+      const ulonglong2 c32 = cs[2 * j], c48 = cs[2 * j + 1];
+      const long long off = a.out_off ? a.out_off[j] : ((long long)j << a.logn);
+#pragma unroll
+      for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // S_b = acc[mb][b >> 1][2h + (b & 1)]
+          const u64 lo = (u64)(u32)acc[mb][0][2 * h] + ((u64)(u32)acc[mb][0][2 * h + 1] << 8) +
+                         ((u64)(u32)acc[mb][1][2 * h] << 16) + ((u64)(u32)acc[mb][1][2 * h + 1] << 24) +
+                         ((u64)(u32)acc[mb][2][2 * h] << 32) + ((u64)(u32)acc[mb][2][2 * h + 1] << 40);
+          const u32 hi = (u32)acc[mb][3][2 * h] + ((u32)acc[mb][3][2 * h + 1] << 8);  // x 2^48
+          u64 r = shoup_lazy32((u32)(lo >> 32), c32.x, c32.y, p) + shoup_lazy32(hi, c48.x, c48.y, p);
+          r = csub(r, 2 * p);
+          r = csub(r, p);
+          r = csub(r + (u32)lo, p);
+          const int row = warp * 32 + mb * 16 + h * 8 + gid;
+          if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[row]], p);
+          if (row0 + row < n) out[off + row0 + row] = r;
+        }
+    }
+  }
+}
+
+template <int KS>
+static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
+  const int n = 1 << G.g[0].logn;
+  const dim3 grid((n + kTcRows - 1) / kTcRows, ng, batch);
+  size_t smem = 0;
+  for (int i = 0; i < ng; ++i) {
+    const BconvArgs& a = G.g[i];
+    const int ntile = ((a.nd + 3) / 4) * 4;
+    const size_t s = (size_t)4 * KS * kTcXs * 8 + (size_t)a.tc_ks * ntile * 32 * sizeof(uint2) +
+                     (size_t)a.nd * (2 * sizeof(ulonglong2) + 8) +
+                     (a.centered ? (size_t)a.nd * (a.ns + 1) * 8 : 0) + kTcRows;
+    smem = s > smem ? s : smem;
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(bconv_tc_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bconv_tc_kernel<KS><<<grid, kTcWarps * 32, smem, st>>>(G);
+}
+
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st) {
   if (ng <= 0 || batch <= 0) return 0;
   if (ng > kMaxBcGroups) return CK_ERR_ARG;
@@ -150,6 +317,20 @@ int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st)
     ns = gs[i].ns > ns ? gs[i].ns : ns;
   }
   count_launches(1);
+  bool tc = true;
+  int tks = 0;
+  for (int i = 0; i < ng; ++i) {
+    tc = tc && gs[i].Bf != nullptr && gs[i].c3248 != nullptr && gs[i].tc_ks >= 1 &&
+         gs[i].tc_ks <= 4 && gs[i].ns <= 4 * gs[i].tc_ks && gs[i].nd <= 64;
+    tks = gs[i].tc_ks > tks ? gs[i].tc_ks : tks;
+  }
+  if (tc) {
+    if (tks <= 1) launch_tc<1>(G, ng, batch, st);
+    else if (tks <= 2) launch_tc<2>(G, ng, batch, st);
+    else if (tks <= 3) launch_tc<3>(G, ng, batch, st);
+    else launch_tc<4>(G, ng, batch, st);
+    return (int)cudaGetLastError();
+  }
   // smallest compiled source count >= ns (extra source rows are zero)
   if (ns <= 1) launch_ns<1>(G, ng, batch, st);
   else if (ns <= 2) launch_ns<2>(G, ng, batch, st);

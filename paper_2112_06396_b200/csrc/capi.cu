@@ -105,6 +105,9 @@ struct ck_bconv {
   int* d_dst = nullptr;
   ulonglong2* d_ihat = nullptr;   // plain ihat (generic apply)
   uint4* d_T = nullptr;
+  uint2* d_Bf = nullptr;          // tensor-core B fragments (bconv_tc_kernel)
+  ulonglong2* d_c3248 = nullptr;
+  int tc_ks = 0;
   double* d_w = nullptr;
   u64* d_kQ = nullptr;
   long long* d_out_off = nullptr; // optional
@@ -152,6 +155,7 @@ struct ck_plan {
   int key_prefetch = 0;    // CKB200_KPF=1: bulk L2 prefetch of key tiles in ks_row (+4 GB DRAM re-reads, measured)
   int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
+  int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
@@ -235,6 +239,52 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
     u64 qm = 1 % pj;
     for (size_t k = 0; k < src.size(); ++k) qm = mulmod_h(qm, p->mod[src[k]] % pj, pj);
     for (size_t k = 0; k <= src.size(); ++k) kQ[j * (src.size() + 1) + k] = mulmod_h(k % pj, qm, pj);
+  }
+  // tensor-core B matrix: B[(i,a)][(j,b)] = byte b of T_ij 2^{8a} mod p_j, in
+  // mma.m16n8k32 fragment order [k-step][n-tile][lane] (see bconv.cu)
+  {
+    const int ns = (int)src.size(), nd = (int)dst.size();
+    const int ks = (ns + 3) / 4, ntile = ((nd + 3) / 4) * 4;
+    std::vector<u64> Tp((size_t)ns * 8 * nd);  // [i][a][j]
+    for (int i = 0; i < ns; ++i)
+      for (int j = 0; j < nd; ++j) {
+        const u64 pj = p->mod[dst[j]];
+        const uint4 q4 = T[(size_t)i * nd + j];
+        const u64 t = (u64)q4.x | ((u64)q4.y << 30);
+        u64 sh = 1 % pj;
+        for (int aa = 0; aa < 8; ++aa) {
+          Tp[((size_t)i * 8 + aa) * nd + j] = mulmod_h(t, sh, pj);
+          sh = mulmod_h(sh, 256 % pj, pj);
+        }
+      }
+    auto byte_at = [&](int k, int col_t, int gid) -> u32 {
+      const int i = k / 8, aa = k % 8;
+      const int g = col_t / 4, u = col_t % 4;
+      const int j = 4 * g + (gid >> 1), bb = 2 * u + (gid & 1);
+      if (i >= ns || j >= nd) return 0;
+      return (u32)((Tp[((size_t)i * 8 + aa) * nd + j] >> (8 * bb)) & 0xff);
+    };
+    std::vector<uint2> Bf((size_t)ks * ntile * 32);
+    for (int s = 0; s < ks; ++s)
+      for (int tt = 0; tt < ntile; ++tt)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int gid = lane >> 2, tig = lane & 3;
+          u32 b0 = 0, b1 = 0;
+          for (int e = 0; e < 4; ++e) {
+            b0 |= byte_at(32 * s + 4 * tig + e, tt, gid) << (8 * e);
+            b1 |= byte_at(32 * s + 16 + 4 * tig + e, tt, gid) << (8 * e);
+          }
+          Bf[((size_t)s * ntile + tt) * 32 + lane] = make_uint2(b0, b1);
+        }
+    std::vector<ulonglong2> c3248((size_t)nd * 2);
+    for (int j = 0; j < nd; ++j) {
+      const u64 pj = p->mod[dst[j]];
+      c3248[2 * j] = sh2(((u64)1 << 32) % pj, pj);
+      c3248[2 * j + 1] = sh2(((u64)1 << 48) % pj, pj);
+    }
+    b->tc_ks = ks;
+    b->d_Bf = upload(b->allocs, Bf, err);
+    b->d_c3248 = upload(b->allocs, c3248, err);
   }
   b->d_src = upload(b->allocs, src, err);
   b->d_dst = upload(b->allocs, dst, err);
@@ -404,6 +454,10 @@ ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, lo
   a.T = bc->d_T;
   a.w = bc->d_w;
   a.kQ = bc->d_kQ;
+  const bool tc = p->bc_tc && bc->tc_ks <= 4 && bc->nd <= 64;
+  a.Bf = tc ? bc->d_Bf : nullptr;
+  a.c3248 = tc ? bc->d_c3248 : nullptr;
+  a.tc_ks = bc->tc_ks;
   a.ns = bc->ns;
   a.nd = bc->nd;
   a.logn = p->logn;
@@ -663,6 +717,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     if (c) p->chunk = atoi(c);
     const char* ns = getenv("CKB200_STREAMS");
     if (ns) p->nstreams = atoi(ns);
+    const char* tc = getenv("CKB200_BCTC");
+    if (tc) p->bc_tc = atoi(tc);
   }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
