@@ -147,18 +147,24 @@ static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 // IMAD pipe that bounds the rest of the key-switch:
 //   x_i        = sum_a x_ia 2^{8a}                 (little-endian bytes, a < 8)
 //   T'_{iaj}   = T_ij 2^{8a} mod p_j = sum_b T'_{iajb} 2^{8b}
-//   S_jb       = sum_{i,a} x_ia T'_{iajb}          (< 64 * 255^2 < 2^22 per 32-byte k-step pair)
+//   S_jb       = sum_{i,a} x_ia T'_{iajb}          (< 128 * 255^2 < 2^23 for <= 4 k-steps)
 //   y_j       == sum_b S_jb 2^{8b}   (mod p_j)
 // A = [coefficients][(i,a)] is the byte view of the u64 source rows (no
 // repacking: a 32-bit A-fragment register is one half of one u64), B =
 // [(i,a)][(j,b)] is precomputed per plan in fragment order.  The n-tiles are
 // arranged so that lane (gid, tig) ends up holding all eight S_jb of target
-// j = 4g + tig for rows gid and gid + 8; the epilogue per (coefficient,
-// target) is two 32x64-bit Shoup products instead of 8 sources x 4 IMAD.WIDE
-// plus a 128-bit reduction.
+// j = 4g + tig for rows gid and gid + 8.
+// Epilogue per (coefficient, target): V = P0 + P1 2^16 + P2 2^32 + P3 2^48
+// (P_k = S_2k + S_2k+1 2^8 < 2^32, V < 2^80); the quotient round(V / p) comes
+// from the FP64 pipe (magic-number conversions, |error| < 2^-16), the
+// remainder from 64-bit integer wrap-around arithmetic, one conditional add.
+// Requires p > 2^50 (quotient < 2^31): checked per conversion at plan time.
+// CTAs loop over kTcTiles row tiles with the next tile's sources staged by
+// cp.async while the current one is on the tensor cores.
 constexpr int kTcWarps = 4;
-constexpr int kTcRows = kTcWarps * 32;  // coefficients per CTA (2 m16 blocks per warp)
+constexpr int kTcRows = kTcWarps * 32;  // coefficients per tile (2 m16 blocks per warp)
 constexpr int kTcXs = kTcRows + 8;      // padded u64 row stride of the staged sources
+constexpr int kTcTiles = 4;             // row tiles per CTA
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) {
   asm volatile(
@@ -168,12 +174,38 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
 }
 
-// x * w mod p in [0, 2p) for x < 2^32 (Shoup, wp = floor(w 2^64 / p))
-__device__ __forceinline__ u64 shoup_lazy32(u32 x, u64 w, u64 wp, u64 p) {
-  const u64 t = (u64)x * (u32)wp;
-  const u64 u = (u64)x * (u32)(wp >> 32) + (t >> 32);
-  const u32 qh = (u32)(u >> 32);
-  return (u64)x * w - (u64)qh * p;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// exact double of a 32-bit integer on the FP64 pipe: bits(0x43300000:v) - 2^52
+__device__ __forceinline__ double u32_to_f64(u32 v) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);
+}
+
+struct TcTarget {
+  u64 p;
+  double pinv;
+  long long off;
+};
+
+template <int KS>
+__device__ __forceinline__ void tc_stage(u64* xs, const BconvArgs& a, const u64* in, int row0,
+                                         int n) {
+  // 4*KS source rows x kTcRows coefficients, 16-byte cp.async chunks
+  constexpr int kChunks = kTcRows / 2;
+  for (int e = threadIdx.x; e < a.ns * kChunks; e += blockDim.x) {
+    const int i = e / kChunks, r = 2 * (e - i * kChunks);
+    u64* dst = xs + i * kTcXs + r;
+    const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
+    if (row0 + r + 1 < n) {
+      cp_async16(dst, in + off + row0 + r);
+    } else {
+      dst[0] = row0 + r < n ? in[off + row0 + r] : 0;
+      dst[1] = 0;
+    }
+  }
 }
 
 template <int KS>
@@ -184,120 +216,137 @@ __global__ void __launch_bounds__(kTcWarps * 32, 4) bconv_tc_kernel(const __grid
   const int ngrp = (nd + 3) >> 2;
   const int ntile = ngrp * 4;
   const int tks = a.tc_ks;
-  u64* xs = (u64*)tc_smem;                                  // [4*KS][kTcXs]
-  uint2* bf = (uint2*)(xs + 4 * KS * kTcXs);                // [tks][ntile][32]
-  ulonglong2* cs = (ulonglong2*)(bf + tks * ntile * 32);    // [nd][2]
-  u64* ps = (u64*)(cs + 2 * nd);                            // [nd]
-  u64* kQs = ps + nd;                                       // [nd][ns+1] (centered)
+  u64* xsb = (u64*)tc_smem;                                 // [2][4*KS][kTcXs]
+  uint2* bf = (uint2*)(xsb + 2 * 4 * KS * kTcXs);           // [tks][ntile][32]
+  TcTarget* tg = (TcTarget*)(bf + tks * ntile * 32);        // [nd]
+  u64* kQs = (u64*)(tg + nd);                               // [nd][ns+1] (centered)
   unsigned char* kk = (unsigned char*)(kQs + (a.centered ? nd * (ns + 1) : 0));  // [kTcRows]
   const int tid = threadIdx.x;
+  const int n = 1 << a.logn;
+  const int ntiles_all = (n + kTcRows - 1) / kTcRows;
+  const int t0 = blockIdx.x * kTcTiles;
+  const int t1 = min(t0 + kTcTiles, ntiles_all);
+  const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
+
+  // zero the padding source rows of both buffers once; stage tile t0
+  for (int e = tid; e < 2 * (4 * KS - ns) * kTcXs; e += blockDim.x) {
+    const int b = e / ((4 * KS - ns) * kTcXs), rem = e - b * ((4 * KS - ns) * kTcXs);
+    xsb[b * 4 * KS * kTcXs + ns * kTcXs + rem] = 0;
+  }
+  tc_stage<KS>(xsb, a, in, t0 * kTcRows, n);
+  cp_async_commit();
   for (int i = tid; i < tks * ntile * 32; i += blockDim.x) bf[i] = a.Bf[i];
   for (int j = tid; j < nd; j += blockDim.x) {
-    cs[2 * j] = a.c3248[2 * j];
-    cs[2 * j + 1] = a.c3248[2 * j + 1];
-    ps[j] = a.pc[a.dst_prime[j]].q;
+    const u64 p = a.pc[a.dst_prime[j]].q;
+    tg[j] = TcTarget{p, 1.0 / (double)p, a.out_off ? a.out_off[j] : ((long long)j << a.logn)};
   }
   if (a.centered)
     for (int i = tid; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
 
-  const int n = 1 << a.logn;
-  const int row0 = blockIdx.x * kTcRows;
-  const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
-  for (int e = tid; e < 4 * KS * kTcRows; e += blockDim.x) {
-    const int i = e / kTcRows, r = e - i * kTcRows;
-    u64 v = 0;
-    if (i < ns && row0 + r < n) {
-      const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
-      v = in[off + row0 + r];
-      if (a.src_scale) {
-        const ulonglong2 sc = a.src_scale[i];
-        v = shoup(v, sc.x, sc.y, a.pc[a.src_prime[i]].q);
-      }
-    }
-    xs[i * kTcXs + r] = v;
-  }
-  __syncthreads();
-  if (a.centered) {
-    // k = rint(sum_i fl(v_i) w_i) in the reference's op order (rnspoly.py:320-325)
-    for (int r = tid; r < kTcRows; r += blockDim.x) {
-      double est = 0.0;
-      for (int i = 0; i < ns; ++i)
-        est = __dadd_rn(est, __dmul_rn(__ull2double_rn(xs[i * kTcXs + r]), a.w[i]));
-      kk[r] = (unsigned char)rint(est);
+  const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
+  u64* out = a.out + (long long)blockIdx.z * a.out_batch;
+  for (int t = t0; t < t1; ++t) {
+    u64* xs = xsb + ((t - t0) & 1) * 4 * KS * kTcXs;
+    if (t + 1 < t1) {
+      tc_stage<KS>(xsb + ((t + 1 - t0) & 1) * 4 * KS * kTcXs, a, in, (t + 1) * kTcRows, n);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-  }
-
-  const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
-  const u32* xw = (const u32*)xs;
-  u32 af[2][KS][4];
-#pragma unroll
-  for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const int r = warp * 32 + mb * 16 + gid;
-      const int i0 = 4 * s + (tig >> 1), i1 = i0 + 2, w = tig & 1;
-      af[mb][s][0] = xw[(i0 * kTcXs + r) * 2 + w];
-      af[mb][s][1] = xw[(i0 * kTcXs + r + 8) * 2 + w];
-      af[mb][s][2] = xw[(i1 * kTcXs + r) * 2 + w];
-      af[mb][s][3] = xw[(i1 * kTcXs + r + 8) * 2 + w];
+    if (a.src_scale) {
+      for (int e = tid; e < ns * kTcRows; e += blockDim.x) {
+        const int i = e / kTcRows, r = e - i * kTcRows;
+        const ulonglong2 sc = a.src_scale[i];
+        xs[i * kTcXs + r] = shoup(xs[i * kTcXs + r], sc.x, sc.y, a.pc[a.src_prime[i]].q);
+      }
+      __syncthreads();
     }
-  u64* out = a.out + (long long)blockIdx.z * a.out_batch;
-  for (int g = 0; g < ngrp; ++g) {
-    int acc[2][4][4];
+    if (a.centered) {
+      // k = rint(sum_i fl(v_i) w_i) in the reference's op order (rnspoly.py:320-325)
+      for (int r = tid; r < kTcRows; r += blockDim.x) {
+        double est = 0.0;
+        for (int i = 0; i < ns; ++i)
+          est = __dadd_rn(est, __dmul_rn(__ull2double_rn(xs[i * kTcXs + r]), a.w[i]));
+        kk[r] = (unsigned char)rint(est);
+      }
+      __syncthreads();
+    }
+    const u32* xw = (const u32*)xs;
+    u32 af[2][KS][4];
 #pragma unroll
     for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[mb][u][c] = 0;
-#pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      if (s < tks) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint2 b = bf[(s * ntile + g * 4 + u) * 32 + lane];
-          mma_u8(acc[0][u], af[0][s], b);
-          mma_u8(acc[1][u], af[1][s], b);
-        }
+      for (int s = 0; s < KS; ++s) {
+        const int r = warp * 32 + mb * 16 + gid;
+        const int i0 = 4 * s + (tig >> 1), i1 = i0 + 2, w = tig & 1;
+        af[mb][s][0] = xw[(i0 * kTcXs + r) * 2 + w];
+        af[mb][s][1] = xw[(i0 * kTcXs + r + 8) * 2 + w];
+        af[mb][s][2] = xw[(i1 * kTcXs + r) * 2 + w];
+        af[mb][s][3] = xw[(i1 * kTcXs + r + 8) * 2 + w];
       }
-    }
-    const int j = g * 4 + tig;
-    if (j < nd) {
-      const u64 p = ps[j];
-      const ulonglong2 c32 = cs[2 * j], c48 = cs[2 * j + 1];
-      const long long off = a.out_off ? a.out_off[j] : ((long long)j << a.logn);
+    const int row0 = t * kTcRows;
+    for (int g = 0; g < ngrp; ++g) {
+      int acc[2][4][4];
 #pragma unroll
       for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          // S_b = acc[mb][b >> 1][2h + (b & 1)]
-          const u64 lo = (u64)(u32)acc[mb][0][2 * h] + ((u64)(u32)acc[mb][0][2 * h + 1] << 8) +
-                         ((u64)(u32)acc[mb][1][2 * h] << 16) + ((u64)(u32)acc[mb][1][2 * h + 1] << 24) +
-                         ((u64)(u32)acc[mb][2][2 * h] << 32) + ((u64)(u32)acc[mb][2][2 * h + 1] << 40);
-          const u32 hi = (u32)acc[mb][3][2 * h] + ((u32)acc[mb][3][2 * h + 1] << 8);  // x 2^48
-          u64 r = shoup_lazy32((u32)(lo >> 32), c32.x, c32.y, p) + shoup_lazy32(hi, c48.x, c48.y, p);
-          r = csub(r, 2 * p);
-          r = csub(r, p);
-          r = csub(r + (u32)lo, p);
-          const int row = warp * 32 + mb * 16 + h * 8 + gid;
-          if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[row]], p);
-          if (row0 + row < n) out[off + row0 + row] = r;
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[mb][u][c] = 0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        if (s < tks) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint2 b = bf[(s * ntile + g * 4 + u) * 32 + lane];
+            mma_u8(acc[0][u], af[0][s], b);
+            mma_u8(acc[1][u], af[1][s], b);
+          }
         }
+      }
+      const int j = g * 4 + tig;
+      if (j < nd) {
+        const TcTarget T = tg[j];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // S_b = acc[mb][b >> 1][2h + (b & 1)];  P_k = S_2k + S_2k+1 2^8
+            const u32 P0 = (u32)acc[mb][0][2 * h] + ((u32)acc[mb][0][2 * h + 1] << 8);
+            const u32 P1 = (u32)acc[mb][1][2 * h] + ((u32)acc[mb][1][2 * h + 1] << 8);
+            const u32 P2 = (u32)acc[mb][2][2 * h] + ((u32)acc[mb][2][2 * h + 1] << 8);
+            const u32 P3 = (u32)acc[mb][3][2 * h] + ((u32)acc[mb][3][2 * h + 1] << 8);
+            // V mod 2^64 and round(V / p) (P0 / p < 2^-18 is dropped from the estimate)
+            const u64 vlo = (u64)P0 + ((u64)P1 << 16) + ((u64)P2 << 32) + ((u64)P3 << 48);
+            const double vd = __fma_rn(u32_to_f64(P3), 281474976710656.0,
+                                       __fma_rn(u32_to_f64(P2), 4294967296.0,
+                                                __dmul_rn(u32_to_f64(P1), 65536.0)));
+            const u32 qh = (u32)__double2loint(__fma_rn(vd, T.pinv, 6755399441055744.0));
+            u64 r = vlo - (u64)qh * T.p;           // in (-p, p) as a signed value
+            r += ((long long)r < 0) ? T.p : 0ull;
+            const int row = warp * 32 + mb * 16 + h * 8 + gid;
+            if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[row]], T.p);
+            if (row0 + row < n) out[T.off + row0 + row] = r;
+          }
+      }
     }
+    __syncthreads();  // xs (and kk) are rewritten by the next iteration's staging
   }
 }
 
 template <int KS>
 static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
   const int n = 1 << G.g[0].logn;
-  const dim3 grid((n + kTcRows - 1) / kTcRows, ng, batch);
+  const int tiles = (n + kTcRows - 1) / kTcRows;
+  const dim3 grid((tiles + kTcTiles - 1) / kTcTiles, ng, batch);
   size_t smem = 0;
   for (int i = 0; i < ng; ++i) {
     const BconvArgs& a = G.g[i];
     const int ntile = ((a.nd + 3) / 4) * 4;
-    const size_t s = (size_t)4 * KS * kTcXs * 8 + (size_t)a.tc_ks * ntile * 32 * sizeof(uint2) +
-                     (size_t)a.nd * (2 * sizeof(ulonglong2) + 8) +
+    const size_t s = (size_t)2 * 4 * KS * kTcXs * 8 + (size_t)a.tc_ks * ntile * 32 * sizeof(uint2) +
+                     (size_t)a.nd * sizeof(TcTarget) +
                      (a.centered ? (size_t)a.nd * (a.ns + 1) * 8 : 0) + kTcRows;
     smem = s > smem ? s : smem;
   }

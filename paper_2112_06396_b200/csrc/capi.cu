@@ -282,7 +282,10 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
       c3248[2 * j] = sh2(((u64)1 << 32) % pj, pj);
       c3248[2 * j + 1] = sh2(((u64)1 << 48) % pj, pj);
     }
-    b->tc_ks = ks;
+    // the FP64 quotient of the epilogue needs every target prime > 2^50
+    bool big = true;
+    for (int j = 0; j < nd; ++j) big = big && p->mod[dst[j]] > ((u64)1 << 50);
+    b->tc_ks = big ? ks : 0;
     b->d_Bf = upload(b->allocs, Bf, err);
     b->d_c3248 = upload(b->allocs, c3248, err);
   }
@@ -454,7 +457,7 @@ ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, lo
   a.T = bc->d_T;
   a.w = bc->d_w;
   a.kQ = bc->d_kQ;
-  const bool tc = p->bc_tc && bc->tc_ks <= 4 && bc->nd <= 64;
+  const bool tc = p->bc_tc && bc->tc_ks >= 1 && bc->tc_ks <= 4 && bc->nd <= 64;
   a.Bf = tc ? bc->d_Bf : nullptr;
   a.c3248 = tc ? bc->d_c3248 : nullptr;
   a.tc_ks = bc->tc_ks;
