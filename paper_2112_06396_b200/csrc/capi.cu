@@ -667,6 +667,8 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ma.x_w = R * N;
   ma.conv_w = l * N;
   ma.out2 = out_b;
+  ma.lazy = 1;
+  for (int k = 0; k < level; ++k) ma.lazy &= p->mod[k] < ((u64)1 << 59) ? 1 : 0;
   return ck::launch_md_row(ma, level, B, st);
 }
 

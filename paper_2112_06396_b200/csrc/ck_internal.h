@@ -74,6 +74,7 @@ struct MdRowArgs {
   int pair;
   long long x_w, conv_w;
   u64* out2;
+  int lazy;                     // every kept prime < 2^59: conv stays lazy (md_row_kernel<.., true>)
 };
 int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st);
 

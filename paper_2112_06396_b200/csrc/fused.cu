@@ -403,7 +403,7 @@ ks_row_ws_kernel(KsRowArgs a, int total_tiles) {
 }
 
 // ------------------------------------------------------------ ModDown row
-template <int P1, int P2>
+template <int P1, int P2, bool LAZY>
 __global__ void __launch_bounds__(FusedCfg<P2>::NT, 8) md_row_kernel(MdRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
@@ -426,9 +426,9 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, 8) md_row_kernel(MdRowArgs a
 #pragma unroll
   for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
   row_transform<P2, false, LOGN>(y, g, r << P2, srow, tw, q, two_q);
-  // conv stays lazy in [0, 16q) when x + 16q - conv fits 64 bits (q < 2^59);
-  // the Shoup multiply below accepts any 64-bit input
-  const bool lazy = q < (1ull << 59);
+  // conv stays lazy in [0, 16q) when x + 16q - conv fits 64 bits (q < 2^59,
+  // LAZY instantiation); the Shoup multiply below accepts any 64-bit input
+  constexpr bool lazy = LAZY;
   if (!lazy) {
 #pragma unroll
     for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
@@ -509,7 +509,9 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
 template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
-  md_row_kernel<P1, P2><<<dim3((1 << P1) / F::TR, batch * (a.pair ? 2 : 1), rows), F::NT, 0, st>>>(a);
+  const dim3 grid((1 << P1) / F::TR, batch * (a.pair ? 2 : 1), rows);
+  if (a.lazy) md_row_kernel<P1, P2, true><<<grid, F::NT, 0, st>>>(a);
+  else md_row_kernel<P1, P2, false><<<grid, F::NT, 0, st>>>(a);
   return 0;
 }
 

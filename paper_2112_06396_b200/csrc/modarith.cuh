@@ -116,7 +116,8 @@ CK_D u32 brev_bits(u32 x, int bits) { return bits ? (__brev(x) >> (32 - bits)) :
 // perm(i) = br(((t * (2 br(i) + 1)) mod 2N - 1) / 2)   (rnspoly.py:127-135).
 CK_D u32 automorph_src(u32 i, u32 t, int logn) {
   u32 j = brev_bits(i, logn);
-  u32 e = (u32)(((u64)t * (2u * j + 1u)) & ((2ull << logn) - 1));
+  // only the product mod 2N <= 2^31 is needed: 32-bit wrap-around IMAD
+  u32 e = (t * (2u * j + 1u)) & ((2u << logn) - 1u);
   return brev_bits((e - 1u) >> 1, logn);
 }
 
