@@ -384,11 +384,14 @@ def mult(params, ct1, ct2, relin):
     return rescale_poly(addmod(b3, u, q2), mods), rescale_poly(addmod(c3, v, q2), mods)
 
 
-def new_mult(params, ct1, ct2, relin, value_mult: int = 1, const_residues=None):
+def new_mult(params, ct1, ct2, relin, value_mult: int = 1, const_residues=None, addend=None):
     """Merged relin ModDown + rescale (ckks.py:603-652).
 
     ``const_residues``: per-limb residues of round(const*delta1*delta2); an
     encoded constant (ckks.py:530-537) is that residue in every eval slot.
+    ``addend``: (a, b, lift) -- ciphertext rows folded in as b3 += a*lift,
+    c3 += b*lift with the signed integer lift round(delta1*delta2/delta_add)
+    (ckks.py:624-636).
     """
     (a1, b1), (a2, b2) = ct1, ct2
     lim = min(a1.shape[0], a2.shape[0])
@@ -399,6 +402,12 @@ def new_mult(params, ct1, ct2, relin, value_mult: int = 1, const_residues=None):
     if value_mult != 1:
         sc = np.array([value_mult % q for q in mods], dtype=U64)[:, None]
         a3, b3, c3 = mulmod(a3, sc, q2), mulmod(b3, sc, q2), mulmod(c3, sc, q2)
+    if addend is not None:
+        ad_a, ad_b, lift = addend
+        assert ad_a.shape[0] >= lim
+        sc = np.array([lift % q for q in mods], dtype=U64)[:, None]
+        b3 = addmod(b3, mulmod(ad_a[:lim], sc, q2), q2)
+        c3 = addmod(c3, mulmod(ad_b[:lim], sc, q2), q2)
     if const_residues is not None:
         c3 = addmod(c3, np.array(const_residues, dtype=U64)[:, None] + np.zeros_like(c3), q2)
     digits = decomp_modup(params, a3, mods)

@@ -63,12 +63,13 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsR
   // Key tiles are only needed after the digit NTTs: start streaming them to L2
   // now (one bulk prefetch per key row-tile, contiguous TR*S words), so the
   // inner product below hits L2 instead of waiting on HBM.
+  // key_prefetch = k: prefetch the first k/8 of each key row-tile (k = 8: all)
   if (a.key_prefetch && threadIdx.x < 2 * beta) {
     const int d = threadIdx.x >> 1;
     const u64* kbase = (threadIdx.x & 1) ? a.key_a : a.key_b;
     prefetch_l2(kbase + b * a.key_batch + d * a.key_digit_stride + ((long long)prime << LOGN) +
                     ((long long)blockIdx.x * F::TR << P2),
-                F::TR * F::S * 8);
+                (F::TR * F::S * 8 / 8) * min(a.key_prefetch, 8));
   }
   if constexpr (BETA > 0) {
     // All digits' source rows are requested up front with async copies into

@@ -65,6 +65,8 @@ def _toy_cases():
             Case(f"{tag}_mult", ps, "mult", (), True),
             Case(f"{tag}_new_mult", ps, "new_mult", (1, None), True),
             Case(f"{tag}_new_mult_vc", ps, "new_mult", (3, 12345), True),
+            Case(f"{tag}_new_mult_add", ps, "new_mult_add", (1, 1, 0), True),
+            Case(f"{tag}_new_mult_sub_lo", ps, "new_mult_add", (5, -1, 1), True),
             Case(f"{tag}_matvec", ps, "pt_matvec", ((0, 1, 3, 5),), True),
         ]
     out.append(Case("B_bsgs", TOY_B, "bsgs", (4, 2), True))
@@ -98,6 +100,9 @@ def all_cases():
 
 def _rows(p: CkksParams, unit: int, tag: int, mods, digit: int = 0, rows=None):
     return synth.uniform_poly(SEED, unit, tag, mods, p.n_ring, digit=digit, rows=rows)
+
+
+ADDEND_DELTA = float(2 ** 30)  # ct deltas are 2^40: lift = round(2^80 / 2^30) = 2^50
 
 
 def _level(p: CkksParams, lv):
@@ -187,6 +192,17 @@ def run_case(case: Case, be):
         vm, const = case.args
         cres = None if const is None else [const % q for q in mods]
         return tuple(be.new_mult(p, ct1, ct2, relin, vm, cres))
+    if op == "new_mult_add":
+        # addend folded in after an integer scale lift (ckks.py:624-636); ct2 may
+        # sit `drop` limbs lower (lim = min, drop_limbs on ct1 and the addend)
+        vm, sign, drop = case.args
+        mods = p.chain
+        ct1 = (_rows(p, 0, synth.TAG_CT_A, mods), _rows(p, 0, synth.TAG_CT_B, mods))
+        m2 = mods[:len(mods) - drop]
+        ct2 = (_rows(p, 0, synth.TAG_CT2_A, m2), _rows(p, 0, synth.TAG_CT2_B, m2))
+        add = (_rows(p, 3, synth.TAG_CT_A, mods), _rows(p, 3, synth.TAG_CT_B, mods))
+        relin = synth.switching_key(p, SEED, 998)
+        return tuple(be.new_mult_add(p, ct1, ct2, relin, vm, add, ADDEND_DELTA, sign))
     if op == "pt_matvec":
         offs = case.args[0]
         mods = p.chain
@@ -211,6 +227,11 @@ def run_case(case: Case, be):
 
 class OracleBackend:
     """The numpy restatement in oracle/ (test infrastructure)."""
+
+    def new_mult_add(self, p, ct1, ct2, relin, vm, add, add_delta, sign):
+        from oracle import ckks_np
+        lift = sign * round(p.delta * p.delta / add_delta)  # ckks.py:632-634
+        return ckks_np.new_mult(p, ct1, ct2, relin, vm, None, addend=(add[0], add[1], lift))
 
     def __getattr__(self, name):
         from oracle import ckks_np

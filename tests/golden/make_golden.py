@@ -118,6 +118,14 @@ class RefBackend:
                           value_mult=vm, const=const)
         return o.a.data, o.b.data
 
+    def new_mult_add(self, p, ct1, ct2, relin, vm, add, add_delta, sign):
+        ks = _keyset(p, relin=_swk(p, *relin))
+        ad = ckks.Ciphertext(_poly(p.chain[:add[0].shape[0]], add[0]),
+                             _poly(p.chain[:add[1].shape[0]], add[1]), add_delta)
+        o = ckks.new_mult(_ref_params(p), ks, self._ct(p, *ct1), self._ct(p, *ct2),
+                          value_mult=vm, addend=ad, addend_sign=sign)
+        return o.a.data, o.b.data
+
     def pt_matvec(self, p, a, b, keys, diags):
         raised = p.raised_moduli(a.shape[0])
         d = {o: _poly(raised, m) for o, m in diags.items()}

@@ -76,6 +76,14 @@ class GpuBackend:
         o = ckks.new_mult(p, ks, _ct(p, *ct1), _ct(p, *ct2), value_mult=vm, const=const)
         return to_host(o.a.data), to_host(o.b.data)
 
+    def new_mult_add(self, p, ct1, ct2, relin, vm, add, add_delta, sign):
+        ks = ckks.KeySet(p, None, ckks.SwitchingKey(p.full_moduli, relin[0], a=relin[1]))
+        ad = ckks.Ciphertext(RnsPoly(p.chain[:add[0].shape[0]], add[0], "eval"),
+                             RnsPoly(p.chain[:add[1].shape[0]], add[1], "eval"), add_delta)
+        o = ckks.new_mult(p, ks, _ct(p, *ct1), _ct(p, *ct2), value_mult=vm, addend=ad,
+                          addend_sign=sign)
+        return to_host(o.a.data), to_host(o.b.data)
+
     def pt_matvec(self, p, a, b, keys, diags):
         raised = p.raised_moduli(a.shape[0])
         d = {o: RnsPoly(raised, m, "eval") for o, m in diags.items()}
