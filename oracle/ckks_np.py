@@ -516,3 +516,17 @@ def expand_key_a(seed: bytes, moduli, digits: int, n: int) -> np.ndarray:
         for i, q in enumerate(moduli):
             a[j, i] = xof_uniform(seed, b"ksk%d:%d" % (j, i), q, n)
     return a
+
+
+def raise_modulus(params, a, b, limbs: int):
+    """ckks.raise_modulus (ckks.py:722-740): centered basis extension of both
+    polynomials from chain[:l] to chain[:limbs] (INTT, centered BC, NTT)."""
+    src = tuple(params.chain[:a.shape[0]])
+    extra = tuple(params.chain[a.shape[0]:limbs])
+    assert a.shape[0] < limbs
+
+    def up(x):
+        conv = ntt(bc_convert_centered(intt(x, src), src, extra), extra)
+        return np.concatenate([x, conv])
+
+    return up(a), up(b)

@@ -484,6 +484,31 @@ def raise_modulus(params: CkksParams, ct: Ciphertext, limbs: int) -> Ciphertext:
     return Ciphertext(up(ct.a), up(ct.b), ct.delta)
 
 
+@dataclass
+class MatvecStage:
+    """bootstrap.MatvecStage (bootstrap.py:212-216): one hoisted linear-transform
+    stage, diagonals {offset: RnsPoly} on the raised basis of entry_limbs."""
+
+    diags: dict
+    diag_delta: float
+    entry_limbs: int
+
+
+def matvec_stages(params: CkksParams, keys: KeySet, ct: Ciphertext, stages) -> Ciphertext:
+    """The CoeffToSlot / SlotToCoeff loops of bootstrap.bootstrap
+    (bootstrap.py:320-321, 329-331): one pt_matvec per stage, each entered at
+    its plan level."""
+    for st in stages:
+        assert ct.limbs == st.entry_limbs, (ct.limbs, st.entry_limbs)
+        ct = pt_matvec(params, keys, ct, st.diags, st.diag_delta)
+    return ct
+
+
+def coeff_to_slot_entry(params: CkksParams, ct: Ciphertext, input_limbs: int) -> Ciphertext:
+    """Bootstrap entry (bootstrap.py:316-318): drop to input_limbs, raise to the top."""
+    return raise_modulus(params, drop_limbs(ct, input_limbs), params.limbs)
+
+
 # ------------------------------------------------------- batched entry
 
 def rotate_batch(params: CkksParams, a: torch.Tensor, b: torch.Tensor, key_b: torch.Tensor,

@@ -152,7 +152,7 @@ struct ck_plan {
   int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
   int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
   int ks_intt_inline = 0;  // CKB200_KSINTT=1: special-row INTT row phase inside ks_row
-  int key_prefetch = 0;    // CKB200_KPF=1: bulk L2 prefetch of key tiles in ks_row (+4 GB DRAM re-reads, measured)
+  int key_prefetch = 2;    // CKB200_KPF=k: L2 prefetch of the first k/8 of each key tile in ks_row (k=8: +4 GB DRAM re-reads; k=2 best, -2%)
   int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
