@@ -30,11 +30,6 @@ struct BcDst {
   u64 p, bar, c30, c30p;
 };
 
-// Several independent conversions (e.g. the beta ModUp digits) share one
-// launch: grid.y selects the group.
-struct BconvGroups {
-  BconvArgs g[kMaxBcGroups];
-};
 
 template <int NS>
 __global__ void __launch_bounds__(kBcThreads, 8) bconv_kernel(const __grid_constant__ BconvGroups G) {

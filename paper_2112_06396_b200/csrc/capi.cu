@@ -156,6 +156,7 @@ struct ck_plan {
   int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
+  int bc_col = 0;     // CKB200_BCCOL=1: conversion fused with the forward column phase (bccol.cu; measured slower)
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
@@ -594,19 +595,27 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
                    a_src, l * N));  // row phase reads the ciphertext directly
   CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, t.d_modup_scale, level, B, l * N, true, 1,
                    st));
+  bool modup_done = false;
   if (t.beta <= ck::kMaxBcGroups) {  // all digits' conversions in one launch
     ck::BconvArgs gs[ck::kMaxBcGroups];
     for (int d = 0; d < t.beta; ++d)
       gs[d] = bconv_args(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
                          false);
-    CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
+    if (p->bc_col && ck::bc_col_supported(gs, t.beta, p->logn)) {
+      // conversion + forward column phase of all targets in one kernel (bccol.cu)
+      CK_TRY(ck::launch_bc_col(gs, t.beta, B, p->d_tw, st));
+      modup_done = true;
+    } else {
+      CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
+    }
   } else {
     for (int d = 0; d < t.beta; ++d)
       CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
                        false, B, st));
   }
-  CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
-                   dig_b, false, 1, st));
+  if (!modup_done)
+    CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs,
+                     B, dig_b, false, 1, st));
   // ---- row phase + automorph + KSKIP (+ INTT row phase of the special rows)
   ck::KsRowArgs ka_;
   ka_.a_eval = a_src;
@@ -642,10 +651,17 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
                    true, p->ks_intt_inline ? 1 : 0, st));
-  CK_TRY(bconv_run(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv, l * N, false, 2 * B,
-                   st));
-  CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false, 1,
-                   st));
+  {
+    const ck::BconvArgs g1 = bconv_args(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv,
+                                        l * N, false);
+    if (p->bc_col && ck::bc_col_supported(&g1, 1, p->logn)) {
+      CK_TRY(ck::launch_bc_col(&g1, 1, 2 * B, p->d_tw, st));
+    } else {
+      CK_TRY(ck::launch_bconv(g1, 2 * B, st));
+      CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false,
+                       1, st));
+    }
+  }
   // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
   ck::MdRowArgs ma;
   ma.prime = m.d_keep_prime;
@@ -724,6 +740,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     if (ns) p->nstreams = atoi(ns);
     const char* tc = getenv("CKB200_BCTC");
     if (tc) p->bc_tc = atoi(tc);
+    const char* bcc = getenv("CKB200_BCCOL");
+    if (bcc) p->bc_col = atoi(bcc);
   }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);

@@ -116,7 +116,16 @@ struct BconvArgs {
 };
 int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st);
 constexpr int kMaxBcGroups = 8;
+// Several independent conversions (e.g. the beta ModUp digits) share one
+// launch: a grid dimension selects the group.
+struct BconvGroups {
+  BconvArgs g[kMaxBcGroups];
+};
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st);
+// conversion fused with the forward NTT column phase of every target (bccol.cu);
+// tw = the plan's forward twiddle table
+bool bc_col_supported(const BconvArgs* gs, int ng, int logn);
+int launch_bc_col(const BconvArgs* gs, int ng, int batch, const ulonglong2* tw, cudaStream_t st);
 
 // Key-switching inner product with a fused eval-domain automorphism.
 struct KskipArgs {
