@@ -326,6 +326,91 @@ def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext,
     return Ciphertext(a_out, b_out, prod_delta / u_hat.moduli[lim - 1])
 
 
+# ------------------------------------------- plaintext-constant operations
+# The sine evaluation of bootstrapping combines new_mult
+# with these.  Constants are encoded on the host exactly as the reference
+# does (Python-int rounding of a float product); everything else runs on the
+# device.
+
+def pt_add(ct: Ciphertext, pt: RnsPoly) -> Ciphertext:
+    """ckks.pt_add (ckks.py:510-511)."""
+    return Ciphertext(ct.a.copy(), ct.b.add(pt), ct.delta)
+
+
+def pt_mult(params: CkksParams, ct: Ciphertext, pt: RnsPoly, pt_delta: float) -> Ciphertext:
+    """ckks.pt_mult (ckks.py:514-518): multiply, then rescale by q_last.
+    (The reference takes no params; the plan is looked up from them here.)"""
+    q_last = ct.a.moduli[-1]
+    return Ciphertext(_rescale_poly_p(params, ct.a.mul(pt)), _rescale_poly_p(params, ct.b.mul(pt)),
+                      ct.delta * pt_delta / q_last)
+
+
+def encode_const(params: CkksParams, c: float, delta: float, moduli) -> RnsPoly:
+    """ckks.encode_const (ckks.py:557-564): round(c*delta) as the degree-0
+    coefficient; its evaluation form is that residue in every slot."""
+    return _const_poly(tuple(moduli), params.n_ring, round(c * delta))
+
+
+def const_add(params: CkksParams, ct: Ciphertext, c: float) -> Ciphertext:
+    """ckks.const_add (ckks.py:567-568)."""
+    return pt_add(ct, encode_const(params, c, ct.delta, ct.a.moduli))
+
+
+def const_mult_int(ct: Ciphertext, c: int) -> Ciphertext:
+    """ckks.const_mult_int (ckks.py:551-554): exact small-integer multiply, no rescale."""
+    scal = [c % q for q in ct.a.moduli]
+    return Ciphertext(ct.a.mul_scalars(scal), ct.b.mul_scalars(scal), ct.delta)
+
+
+_MONO_CACHE: dict = {}
+
+
+def monomial(params: CkksParams, k: int, moduli) -> RnsPoly:
+    """ckks.monomial (ckks.py:574-582): X^k in evaluation form (device NTT of e_k)."""
+    moduli = tuple(moduli)
+    key = (params.logn, k, moduli)
+    if key not in _MONO_CACHE:
+        data = torch.zeros((len(moduli), params.n_ring), dtype=torch.uint64, device="cuda")
+        data[:, k] = 1
+        _MONO_CACHE[key] = RnsPoly(moduli, data, "coeff").to_eval()
+    return _MONO_CACHE[key]
+
+
+def mult_monomial(params: CkksParams, ct: Ciphertext, k: int) -> Ciphertext:
+    """ckks.mult_monomial (ckks.py:585-588): multiply by X^k (exact, depth-free)."""
+    mono = monomial(params, k, ct.a.moduli)
+    return Ciphertext(ct.a.mul(mono), ct.b.mul(mono), ct.delta)
+
+
+def pt_combo(params: CkksParams, terms, const: float = 0.0) -> Ciphertext:
+    """ckks.pt_combo (ckks.py:521-548): sum_j c_j ct_j + const with one shared
+    rescale; each slot-constant c_j is encoded at scale S / ct_j.delta.
+    Slot-vector coefficients need the host encoder (out of scope): pass a
+    pre-encoded RnsPoly on the combined basis instead."""
+    assert terms
+    lim = min(ct.limbs for ct, _ in terms)
+    mods = terms[0][0].a.moduli[:lim]
+    s_pre = params.delta * terms[0][0].delta
+    acc_a = RnsPoly.zeros(mods, params.n_ring, "eval")
+    acc_b = RnsPoly.zeros(mods, params.n_ring, "eval")
+    for ct, c in terms:
+        ct = drop_limbs(ct, lim)
+        if isinstance(c, RnsPoly):
+            ta, tb = ct.a.mul(c), ct.b.mul(c)
+        else:
+            assert not isinstance(c, np.ndarray), "slot-vector encode is host-side; pass an RnsPoly"
+            # a slot constant's evaluation form is one residue per limb
+            v = round(c * (s_pre / ct.delta))
+            scal = [v % q for q in mods]
+            ta, tb = ct.a.mul_scalars(scal), ct.b.mul_scalars(scal)
+        acc_a = acc_a.add(ta)
+        acc_b = acc_b.add(tb)
+    if const:
+        acc_b = acc_b.add(encode_const(params, const, s_pre, mods))
+    return Ciphertext(_rescale_poly_p(params, acc_a), _rescale_poly_p(params, acc_b),
+                      s_pre / mods[-1])
+
+
 def hrotate(params: CkksParams, keys: KeySet, ct: Ciphertext, rotations) -> list[Ciphertext]:
     """ckks.hrotate (ckks.py:655-667): one shared ModUp, all KSKIPs in one
     launch, batched ModDown pairs -- a single ck_hrotate call."""
