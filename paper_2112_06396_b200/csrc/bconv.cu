@@ -153,7 +153,8 @@ static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 // (P_k = S_2k + S_2k+1 2^8 < 2^32, V < 2^80); the quotient round(V / p) comes
 // from the FP64 pipe (magic-number conversions, |error| < 2^-16), the
 // remainder from 64-bit integer wrap-around arithmetic, one conditional add.
-// Requires p > 2^50 (quotient < 2^31): checked per conversion at plan time.
+// Requires V / p < 2^31 (the quotient is read from 31 mantissa bits): the plan
+// checks the bound per conversion (any target above ~2^48 qualifies).
 // CTAs loop over kTcTiles row tiles with the next tile's sources staged by
 // cp.async while the current one is on the tensor cores.
 constexpr int kTcWarps = 4;
