@@ -61,11 +61,13 @@ class CkError(RuntimeError):
     pass
 
 
-def load(path: str = LIB_PATH):
-    """Load the shared library (no device needed) and bind every symbol."""
+def load(path: str | None = None):
+    """Load the shared library (no device needed) and bind every symbol.
+    CKB200_LIB overrides the path (A/B builds of the same sources)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("CKB200_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise CkError(f"{path} missing: run `python -m paper_2112_06396_b200.build` "
                       "(there is no CPU fallback)")

@@ -28,14 +28,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
+    """Compile every source and link `out`.  `extra` nvcc flags build A/B
+    variants (e.g. -DCKB200_EXACT_SHOUP into another .so, selected at run time
+    with CKB200_LIB=<path>)."""
+    if out == LIB and not extra and not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        tag = os.path.basename(out).replace(".so", "")
+        obj = os.path.join(CSRC, src.replace(".cu", f".{tag}.o"))
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     objs = []
@@ -47,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
             objs.append(obj)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", out,
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -55,8 +59,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("link failed")
     for o in objs:
         os.remove(o)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = [a for a in sys.argv[1:] if a not in ("--force", "-v")]
+    flags = [a for a in args if a.startswith("-D")]
+    outs = [a for a in args if a.endswith(".so")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, extra=flags,
+                out=os.path.abspath(outs[0]) if outs else LIB))

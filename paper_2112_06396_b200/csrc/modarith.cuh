@@ -38,6 +38,27 @@ CK_D u64 shoup_lazy(u64 x, u64 w, u64 wp, u64 q) {
 
 CK_D u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
 
+// NTT twiddle product in [0, 2q) for any 64-bit x (same contract as
+// shoup_lazy).  The Shoup quotient drops x0*wp0 and the low halves of the
+// two cross products: qa = x1 wp1 + hi(x1 wp0) + hi(x0 wp1) is at most 2
+// below floor(x wp / 2^64), so x w - qa q lies in [0, 4q) and one csub(2q)
+// restores [0, 2q).  Integer cost: 2 IMAD.HI + 1 IMAD.WIDE for the quotient
+// instead of a full 64x64 mulhi (4 IMAD.WIDE + carries); the correction runs
+// on the ALU pipe.  Needs q < 2^62.  Measured 39% SLOWER on C3 (the extra
+// live values push the 64-register NTT kernels into local-memory spills), so
+// it is opt-in (-DCKB200_APPROX_SHOUP); the default is the exact Shoup product.
+CK_D u64 madw(u32 a, u32 b, u64 acc);
+CK_D u64 shoup_tw(u64 x, u64 w, u64 wp, u64 q, u64 two_q) {
+#ifdef CKB200_APPROX_SHOUP
+  const u32 x0 = (u32)x, x1 = (u32)(x >> 32), p0 = (u32)wp, p1 = (u32)(wp >> 32);
+  const u64 qa = madw(x1, p1, (u64)__umulhi(x1, p0)) + __umulhi(x0, p1);
+  const u64 r = x * w - qa * q;
+  return r >= two_q ? r - two_q : r;
+#else
+  return x * w - __umul64hi(x, wp) * q;
+#endif
+}
+
 CK_D u64 shoup(u64 x, u64 w, u64 wp, u64 q) { return csub(shoup_lazy(x, w, wp, q), q); }
 
 CK_D u64 addmod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
@@ -98,7 +119,7 @@ CK_D u64 acc3_reduce(const Acc3& s, const PrimeConst& P) {
 // Forward CT: X, Y in [0, 4q) -> [0, 4q).
 CK_D void bfly_ct(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
   u64 x = csub(X, two_q);
-  u64 t = shoup_lazy(Y, w, wp, q);
+  u64 t = shoup_tw(Y, w, wp, q, two_q);
   X = x + t;
   Y = x - t + two_q;
 }
@@ -106,7 +127,7 @@ CK_D void bfly_ct(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
 CK_D void bfly_gs(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
   u64 x = X, y = Y;
   X = csub(x + y, two_q);
-  Y = shoup_lazy(x - y + two_q, w, wp, q);
+  Y = shoup_tw(x - y + two_q, w, wp, q, two_q);
 }
 
 // ---- index helpers ----

@@ -100,7 +100,7 @@ CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict_
           if (INV) {
             bfly_gs(X, Y, w.x, w.y, q, two_q);
           } else {
-            const u64 t = shoup_lazy(Y, w.x, w.y, q);
+            const u64 t = shoup_tw(Y, w.x, w.y, q, two_q);
             const u64 xx = X;
             X = xx + t;
             Y = xx - t + two_q;
@@ -266,7 +266,7 @@ CK_D void run_pass_rs(u64 (&x)[kE], int g, int rl, const ulonglong2* __restrict_
           if (INV) {
             bfly_gs(X, Y, w.x, w.y, q, two_q);
           } else {
-            const u64 t = shoup_lazy(Y, w.x, w.y, q);
+            const u64 t = shoup_tw(Y, w.x, w.y, q, two_q);
             const u64 xx = X;
             X = xx + t;
             Y = xx - t + two_q;
