@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libckks_b200.so")
-SOURCES = ["ntt.cu", "bconv.cu", "bccol.cu", "kskip.cu", "ew.cu", "fused.cu", "bsgs.cu", "xof.cu", "capi.cu"]
+SOURCES = ["ntt.cu", "ntt_tc.cu", "bconv.cu", "bccol.cu", "kskip.cu", "ew.cu", "fused.cu", "bsgs.cu", "xof.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -161,6 +161,9 @@ constexpr int kTcWarps = 4;
 constexpr int kTcRows = kTcWarps * 32;  // coefficients per tile (2 m16 blocks per warp)
 constexpr int kTcXs = kTcRows + 8;      // padded u64 row stride of the staged sources
 constexpr int kTcTiles = 4;             // row tiles per CTA
+#ifndef CKB200_BCTC_MINB
+#define CKB200_BCTC_MINB 4                // resident CTAs per SM the registers are sized for
+#endif
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) {
   asm volatile(
@@ -205,7 +208,7 @@ __device__ __forceinline__ void tc_stage(u64* xs, const BconvArgs& a, const u64*
 }
 
 template <int KS>
-__global__ void __launch_bounds__(kTcWarps * 32, 4) bconv_tc_kernel(const __grid_constant__ BconvGroups G) {
+__global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kernel(const __grid_constant__ BconvGroups G) {
   const BconvArgs& a = G.g[blockIdx.y];
   extern __shared__ __align__(16) unsigned char tc_smem[];
   const int nd = a.nd, ns = a.ns;

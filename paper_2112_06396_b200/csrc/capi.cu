@@ -157,6 +157,8 @@ struct ck_plan {
   int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
   int bc_col = 0;     // CKB200_BCCOL=1: conversion fused with the forward column phase (bccol.cu; measured slower)
+  unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
+  ulonglong2* d_tcD = nullptr;
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
@@ -423,6 +425,8 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
   a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
+  a.tcB = p->d_tcB;
+  a.tcD = p->d_tcD;
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
 
@@ -443,6 +447,8 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
   a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
+  a.tcB = p->d_tcB;
+  a.tcD = p->d_tcD;
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
 
@@ -816,6 +822,17 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   {
     const char* e = getenv("CKB200_FPNTT");
     p->fp_ntt = e && e[0] == '1';
+  }
+  if (log_n == 16 || log_n == 17) {
+    const char* e = getenv("CKB200_NTTTC");
+    if (!(e && e[0] == '0')) {
+      std::vector<unsigned char> tb;
+      std::vector<ulonglong2> td;
+      if (ck::ntt_tc_tables(p->mod.data(), np, tw.data(), N, tb, td)) {
+        p->d_tcB = upload(p->allocs, tb, &err);
+        p->d_tcD = upload(p->allocs, td, &err);
+      }
+    }
   }
   p->lv.resize(n_chain + 1);
   for (int l = 1; l <= n_chain && !err; ++l) err = build_level(p, l);

@@ -211,7 +211,9 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
   count_launches((int)col + (int)row);
   const bool fp = a.ctw != nullptr;
   if (!inv) {
-    if (col) {
+    if (col && P1 == 8 && a.tcB && launch_ntt_col_tc(a, jobs, batch, st) == 0) {
+      // forward column phase ran on the tensor cores (ntt_tc.cu)
+    } else if (col) {
       if (fp) ntt_col_kernel<P1, P2, false, true><<<gcol, bcol, 0, st>>>(a);
       else ntt_col_kernel<P1, P2, false, false><<<gcol, bcol, 0, st>>>(a);
     }

@@ -40,6 +40,9 @@ struct NttArgs {
   const Tw4* ctw;              // column-phase twiddles in FP64-assisted form,
   const Tw4* citw;             //   [prime][2^P1] (nullable: integer Shoup path)
   int logn;
+  // tensor-core forward column phase (ntt_tc.cu; nullable: butterfly kernels)
+  const unsigned char* tcB = nullptr;  // [prime][2][128 x 128 B] B1 | B2 in SMEM layout
+  const ulonglong2* tcD = nullptr;     // [prime][16][16] twists {d, d_shoup}
 };
 
 // ---- compile-time pass schedule for a 2^P-point sub-transform ----

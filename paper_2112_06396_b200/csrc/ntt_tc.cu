@@ -1,0 +1,363 @@
+// Forward NTT column phase on the 5th-generation tensor cores (tcgen05.mma
+// kind::i8, accumulators in TMEM).
+//
+// The column phase (stages m = 1 .. 128 of the reference's Cooley-Tukey
+// ladder, rnspoly.py:48-62, on the 256 x 2^P2 storage matrix) maps every
+// column c through the SAME 256 x 256 matrix.  Split by row bits
+// r = 16 r_hi + r_lo:
+//   stages m = 1..8   mix r_hi only, with twiddles that depend on r_hi alone:
+//                     one 16 x 16 matrix M1, shared by every (r_lo, c);
+//   stages m = 16..128 mix r_lo inside block beta = r_hi; that block evaluates
+//                     mod (X^16 - gamma_beta), i.e. M2[beta] = F diag(d_beta)
+//                     with F = M2[0] and a per-(beta, r_lo) twist d_beta
+//                     (the plan derives F and d from the twiddle table and
+//                     verifies the factorisation entry by entry).
+// Each 16-point product is an exact integer GEMM on bytes: with x = sum_a
+// x_a 2^8a and B[(j,a)][(k,b)] = byte b of (Mat[k][j] 2^8a mod p),
+//   S_kb = sum_(j,a) x_ja B[(j,a)][(k,b)]     (K = 128 bytes, < 2^23)
+//   y_k == sum_b S_kb 2^8b  (mod p)
+// so no modular reduction is needed inside the GEMM, any 64-bit input is
+// allowed, and the epilogue reduces V = sum_b S_kb 2^8b < 2^80 once (FP64
+// quotient, as in the tensor-core base conversion).
+//
+// CTA = 16 columns x 256 rows of one limb (32 KB), 256 threads:
+//   load tile -> A1[(r_lo,c)][r_hi]        (256 x 128 B, canonical K-major)
+//   MMA  D1 = A1 . B1^T                     (2 x M128 N128 K128, TMEM cols 0..255)
+//   epilogue: y = (V mod p) * d_beta[r_lo]  -> A2[(beta,c)][r_lo]
+//   MMA  D2 = A2 . B2^T
+//   epilogue: V mod p, lazy in (0, 2p)      -> global rows 16 beta + k
+// Output is lazy in (0, 2p) (the butterfly kernels leave [0, 16q)); every
+// consumer folds either.
+#include "ck_internal.h"
+#include "ntt.cuh"
+
+#include <vector>
+
+namespace ck {
+
+namespace {
+
+constexpr int kTcCols = 8;                   // columns per tile (M = 16 x 8 = 128 rows)
+constexpr int kTcGroups = 4;                 // independent 8-warp pipelines per CTA (share B)
+constexpr int kTcGW = 8;                     // warps per group: 2 per TMEM lane quarter
+constexpr int kTcThreads = 32 * kTcGW * kTcGroups;
+#ifndef CKB200_TC_TILES
+#define CKB200_TC_TILES 32
+#endif
+constexpr int kTcTiles = CKB200_TC_TILES;    // tiles per CTA (B loaded once per CTA)
+constexpr int kOpBytes = 128 * 128;          // one 128-row operand (A), bytes
+constexpr int kBBytes = 128 * 128;           // one B matrix (N = 128 rows of K = 128 bytes)
+
+// Canonical K-major SWIZZLE_NONE layout of rows of 128 bytes: 8x16-byte core
+// matrices, LBO = 128 B between K chunks, SBO = 1024 B between 8-row groups.
+__host__ __device__ __forceinline__ unsigned kmaj_off(int row, int byte) {
+  return ((((unsigned)row >> 3) * 8u + ((unsigned)byte >> 4)) << 7) + (((unsigned)row & 7u) << 4) +
+         ((unsigned)byte & 15u);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(unsigned saddr) {
+  const uint64_t lbo = 128 >> 4, sbo = 1024 >> 4;
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (lbo << 16) | (sbo << 32) | (1ull << 46);
+}
+
+// kind::i8, A/B unsigned 8-bit, D s32, K-major A and B, M = 128, N = 128
+constexpr uint32_t kIdesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// V = sum_b S_b 2^8b (S_b < 2^23, V < 2^80) reduced into (0, 2p), p > 2^49.5:
+// quotient qh = round(vhi 2^32 / p) from vhi = floor(V / 2^32) (exact in a
+// double); the dropped low part adds < 2^48 / p < 0.36 to the error, so
+// |V/p - qh| < 1 and V - qh p + p lands in (0, 2p), computed mod 2^64.
+__device__ __forceinline__ u64 reduce_lazy(const uint32_t* s, u64 p, double pinv32) {
+  const u32 P0 = s[0] + (s[1] << 8), P1 = s[2] + (s[3] << 8);
+  const u32 P2 = s[4] + (s[5] << 8), P3 = s[6] + (s[7] << 8);
+  const u64 vlo = (u64)P0 + ((u64)P1 << 16) + ((u64)P2 << 32) + ((u64)P3 << 48);
+  const u64 vhi = ((u64)P3 << 16) + P2;  // < 2^49
+  const double vd = __dsub_rn(__longlong_as_double((long long)(vhi | 0x4330000000000000ull)),
+                              4503599627370496.0);
+  const u32 qh = (u32)__double2loint(__fma_rn(vd, pinv32, 6755399441055744.0));
+  return vlo - (u64)qh * p + p;
+}
+
+__device__ __forceinline__ void st_u64(unsigned char* base, int row, int elem, u64 v) {
+  *(u64*)(base + kmaj_off(row, elem * 8)) = v;
+}
+
+// Tile t's 256 x 8 block goes straight from global memory into operand
+// layout with 8-byte cp.async (no registers): lane -> (c = lane & 7,
+// r_hi = 4 warp + lane / 8), iteration -> r_lo.  A warp's 32 copies land in
+// two 128-byte core-matrix rows (no bank conflicts) and read 4 x 64-byte
+// row segments.
+template <int P2>
+__device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int c0, int gw, int lane) {
+  const int c = lane & 7, r_hi = 4 * (gw & 3) + (lane >> 3);   // gw: warp within the group
+#pragma unroll
+  for (int r_lo = 8 * (gw >> 2); r_lo < 8 * (gw >> 2) + 8; ++r_lo) {
+    const u64* src = base + ((long long)(r_hi * 16 + r_lo) << P2) + c0 + c;
+    const unsigned dst = a_dst + kmaj_off(8 * r_lo + c, 8 * r_hi);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Four 8-warp groups per CTA (one CTA per SM: 512 TMEM columns, 32 warps)
+// run independent tile pipelines (own double-buffered A operand, TMEM
+// accumulator, mbarrier and named barrier) over tiles g, g+4, ...,
+// sharing the CTA's B matrices and twists.  Tile t+4's data streams in
+// (cp.async) while tile t is on the tensor cores and in the epilogues; the
+// two warps of a TMEM lane quarter split each epilogue's 16 outputs.
+template <int P2>
+__global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  unsigned char* Bm = tsm + 2 * kTcGroups * kOpBytes;      // A[group][2] (16 KB each), then B1 | B2
+  ulonglong2* tw = (ulonglong2*)(Bm + 2 * kBBytes);        // twists [beta][r_lo] (4 KB)
+  uint64_t* mbar = (uint64_t*)(tw + 256);                  // [group]
+  uint32_t* tslot = (uint32_t*)(mbar + kTcGroups);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = warp / kTcGW, gw = warp % kTcGW, gtid = tid % (32 * kTcGW);
+  const int quarter = gw & 3, half = gw >> 2;
+  const int job = blockIdx.y;
+  const int prime = a.prime_idx[job];
+  const u64 p = a.pc[prime].q;
+  const double pinv32 = __drcp_rn((double)p) * 4294967296.0;  // 2^32 / p
+  u64* base = a.data + (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) +
+              (long long)blockIdx.z * a.batch_stride;
+  const unsigned mb_s = (unsigned)__cvta_generic_to_shared(mbar + grp);
+  const unsigned abuf_s = (unsigned)__cvta_generic_to_shared(tsm) + grp * 2 * kOpBytes;
+  unsigned char* abuf = tsm + grp * 2 * kOpBytes;
+  const unsigned b_s = (unsigned)__cvta_generic_to_shared(Bm);
+  const int cbase = blockIdx.x * kTcTiles * kTcCols;
+  const int bar_id = 1 + grp;
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kTcGW) : "memory"); };
+
+  stage_tile<P2>(abuf_s, base, cbase + grp * kTcCols, gw, lane);      // this group's first tile
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        (unsigned)__cvta_generic_to_shared(tslot)), "n"(128 * kTcGroups));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (gtid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s));
+  {
+    const uint4* src = (const uint4*)(a.tcB + (size_t)prime * 2 * kBBytes);
+    uint4* dst = (uint4*)Bm;
+    for (int i = tid; i < 2 * kBBytes / 16; i += kTcThreads) dst[i] = __ldg(src + i);
+    const ulonglong2* ts = a.tcD + (size_t)prime * 256;
+    for (int i = tid; i < 256; i += kTcThreads) tw[i] = __ldg(ts + i);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tacc = *tslot + grp * 128;                     // this group's accumulator columns
+  const uint32_t tl = tacc + ((uint32_t)(quarter * 32) << 16);  // this warp's lane quarter
+  const int m = quarter * 32 + lane;                            // this thread's D row
+  unsigned phase = 0;
+
+  for (int it = 0; grp + kTcGroups * it < kTcTiles; ++it) {
+    const int tile = grp + kTcGroups * it;
+    const int c0 = cbase + tile * kTcCols;
+    unsigned char* A = abuf + (it & 1) * kOpBytes;
+    const unsigned a_s = abuf_s + (it & 1) * kOpBytes;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    fence_async_smem();
+    tc_fence_before();
+    gsync();
+    tc_fence_after();
+    if (tile + kTcGroups < kTcTiles)
+      stage_tile<P2>(abuf_s + ((it + 1) & 1) * kOpBytes, base, c0 + kTcGroups * kTcCols, gw, lane);
+    // ---- pass 1: D1[(r_lo,c)][(beta,b)] = A1 . B1^T
+    if (gtid == 0) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) mma_i8(tacc, smem_desc(a_s + s * 256), smem_desc(b_s + s * 256), s > 0);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_s)
+                   : "memory");
+    }
+    mbar_wait(mb_s, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      const int r_lo = m >> 3, c = m & 7;
+#pragma unroll 1
+      for (int h = 2 * half; h < 2 * half + 2; ++h) {   // 4 outputs (32 TMEM columns) per wait
+        uint32_t sv[32];
+        tmem_ld32(tl + h * 32, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int beta = h * 4 + u;
+          const u64 y = reduce_lazy(sv + 8 * u, p, pinv32);
+          const ulonglong2 d = tw[beta * 16 + r_lo];
+          st_u64(A, beta * 8 + c, r_lo, shoup_lazy(y, d.x, d.y, p));  // [0, 2p)
+        }
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    gsync();
+    tc_fence_after();
+    // ---- pass 2: D2[(beta,c)][(k,b)] = A2 . B2^T
+    if (gtid == 0) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        mma_i8(tacc, smem_desc(a_s + s * 256), smem_desc(b_s + kBBytes + s * 256), s > 0);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb_s)
+                   : "memory");
+    }
+    mbar_wait(mb_s, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      const int beta = m >> 3, c = m & 7;
+      u64* col = base + c0 + c;
+#pragma unroll 1
+      for (int h = 2 * half; h < 2 * half + 2; ++h) {
+        uint32_t sv[32];
+        tmem_ld32(tl + h * 32, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          col[(long long)(beta * 16 + h * 4 + u) << P2] = reduce_lazy(sv + 8 * u, p, pinv32);
+      }
+    }
+    tc_fence_before();   // the next tile's MMA rewrites D: TMEM reads are complete
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(128 * kTcGroups));
+  }
+}
+
+constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 64;
+
+template <int P2>
+int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ntt_col_tc_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTcSmem);
+    attr = true;
+  }
+  const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
+  ntt_col_tc_kernel<P2><<<grid, kTcThreads, kTcSmem, st>>>(a);
+  return 0;
+}
+
+// ---------------------------------------------------------------- host side
+using u128 = unsigned __int128;
+u64 mm(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+u64 pw(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q;
+  for (; e; e >>= 1, a = mm(a, a, q))
+    if (e & 1) r = mm(r, a, q);
+  return r;
+}
+
+// Run CT stages s in [s0, s1) of the 256-row column phase on a 256-vector.
+void col_stages(std::vector<u64>& x, const ulonglong2* tw, u64 q, int s0, int s1) {
+  for (int s = s0; s < s1; ++s) {
+    const int m = 1 << s, t = 128 >> s;
+    for (int i = 0; i < m; ++i) {
+      const u64 w = tw[m + i].x;
+      for (int j = i * 2 * t; j < i * 2 * t + t; ++j) {
+        const u64 u = x[j], v = mm(x[j + t], w, q);
+        x[j] = (u + v) % q;
+        x[j + t] = (u + q - v) % q;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool ntt_tc_tables(const u64* mod, int np, const ulonglong2* tw_host, long long n,
+                   std::vector<unsigned char>& B, std::vector<ulonglong2>& D) {
+  B.assign((size_t)np * 2 * kBBytes, 0);
+  D.assign((size_t)np * 256, make_ulonglong2(0, 0));
+  for (int pi = 0; pi < np; ++pi) {
+    const u64 q = mod[pi];
+    if ((double)q < 796131459065721.0) return false;  // reduce_lazy needs p > 2^49.5
+    const ulonglong2* tw = tw_host + (size_t)pi * n;
+    u64 M1[16][16], M2[16][16][16];  // M2[beta][k][j]
+    for (int j = 0; j < 16; ++j) {
+      std::vector<u64> x(256, 0);
+      x[16 * j] = 1;
+      col_stages(x, tw, q, 0, 4);
+      for (int k = 0; k < 16; ++k) M1[k][j] = x[16 * k];
+      for (int beta = 0; beta < 16; ++beta) {
+        std::vector<u64> y(256, 0);
+        y[16 * beta + j] = 1;
+        col_stages(y, tw, q, 4, 8);
+        for (int k = 0; k < 16; ++k) M2[beta][k][j] = y[16 * beta + k];
+        // M1 must not leak across r_lo, nor M2 across blocks
+        for (int r = 0; r < 256; ++r)
+          if ((r >> 4) != beta && y[r]) return false;
+      }
+    }
+    // F = M2[0]; twist d_beta[j] = M2[beta][0][j] / F[0][j]; verify M2[beta] = F diag(d_beta)
+    for (int beta = 0; beta < 16; ++beta)
+      for (int j = 0; j < 16; ++j) {
+        if (M2[0][0][j] == 0) return false;
+        const u64 d = mm(M2[beta][0][j], pw(M2[0][0][j], q - 2, q), q);
+        for (int k = 0; k < 16; ++k)
+          if (mm(M2[0][k][j], d, q) != M2[beta][k][j]) return false;
+        D[(size_t)pi * 256 + beta * 16 + j] = make_ulonglong2(d, (u64)(((u128)d << 64) / q));
+      }
+    // B matrices: B[n = 8k + b][byte 8j + a] = byte b of (Mat[k][j] 2^8a mod q)
+    for (int which = 0; which < 2; ++which) {
+      unsigned char* dst = B.data() + ((size_t)pi * 2 + which) * kBBytes;
+      for (int k = 0; k < 16; ++k)
+        for (int j = 0; j < 16; ++j) {
+          u64 v = which == 0 ? M1[k][j] : M2[0][k][j];
+          for (int aa = 0; aa < 8; ++aa) {
+            for (int b = 0; b < 8; ++b) dst[kmaj_off(8 * k + b, 8 * j + aa)] = (unsigned char)(v >> (8 * b));
+            v = mm(v, 256 % q, q);
+          }
+        }
+    }
+  }
+  return true;
+}
+
+// Forward column phase on the tensor cores (P1 = 8 only); -1 if not applicable.
+int launch_ntt_col_tc(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
+  if (!a.tcB || !a.tcD) return -1;
+  switch (a.logn) {
+    case 16: return launch_t<8>(a, jobs, batch, st);
+    case 17: return launch_t<9>(a, jobs, batch, st);
+    default: return -1;
+  }
+}
+
+}  // namespace ck
