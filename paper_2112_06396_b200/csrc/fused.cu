@@ -405,7 +405,10 @@ ks_row_ws_kernel(KsRowArgs a, int total_tiles) {
 
 // ------------------------------------------------------------ ModDown row
 template <int P1, int P2, bool LAZY>
-__global__ void __launch_bounds__(FusedCfg<P2>::NT, 8) md_row_kernel(MdRowArgs a) {
+#ifndef CKB200_MD_MINB
+#define CKB200_MD_MINB 8
+#endif
+__global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
   __shared__ u64 stage[F::TR * F::RS];

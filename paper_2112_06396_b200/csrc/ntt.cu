@@ -12,8 +12,11 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 
 // ------------------------------------------------------------ column phase
 // grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
+#ifndef CKB200_NTT_MINB
+#define CKB200_NTT_MINB 3
+#endif
 template <int P1, int P2, bool INV, bool FP>
-__global__ void __launch_bounds__(kTC * (1 << P1) / kE, FP ? 3 : 4)
+__global__ void __launch_bounds__(kTC * (1 << P1) / kE, FP ? 3 : CKB200_NTT_MINB)
 ntt_col_kernel(NttArgs a) {
   constexpr int S = 1 << P1;
   constexpr int NP = Sched<P1>::np;
@@ -85,7 +88,7 @@ struct RowCfg {
 };
 
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, CKB200_NTT_MINB)
 ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;
