@@ -159,6 +159,7 @@ struct ck_plan {
   int bc_col = 0;     // CKB200_BCCOL=1: conversion fused with the forward column phase (bccol.cu; measured slower)
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
   ulonglong2* d_tcD = nullptr;
+  int ntt_tc_inv = 1;  // CKB200_NTTTC=2: forward column phase only on the tensor cores
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
@@ -427,6 +428,7 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   a.logn = p->logn;
   a.tcB = p->d_tcB;
   a.tcD = p->d_tcD;
+  a.tc_inv = p->ntt_tc_inv;
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
 
@@ -449,6 +451,7 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   a.logn = p->logn;
   a.tcB = p->d_tcB;
   a.tcD = p->d_tcD;
+  a.tc_inv = p->ntt_tc_inv;
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
 
@@ -825,10 +828,11 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   }
   if (log_n == 16 || log_n == 17) {
     const char* e = getenv("CKB200_NTTTC");
+    p->ntt_tc_inv = !(e && e[0] == '2');
     if (!(e && e[0] == '0')) {
       std::vector<unsigned char> tb;
       std::vector<ulonglong2> td;
-      if (ck::ntt_tc_tables(p->mod.data(), np, tw.data(), N, tb, td)) {
+      if (ck::ntt_tc_tables(p->mod.data(), np, tw.data(), itw.data(), N, tb, td)) {
         p->d_tcB = upload(p->allocs, tb, &err);
         p->d_tcD = upload(p->allocs, td, &err);
       }

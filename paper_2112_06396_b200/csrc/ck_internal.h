@@ -31,10 +31,10 @@ bool fused_supported(int logn);
 // tensor-core forward column phase (ntt_tc.cu): tables per plan prime, launch
 // (returns -1 when the shape is not covered; the caller uses the butterflies)
 #ifdef __CUDACC__
-bool ntt_tc_tables(const u64* mod, int np, const ulonglong2* tw_host, long long n,
-                   std::vector<unsigned char>& B, std::vector<ulonglong2>& D);
+bool ntt_tc_tables(const u64* mod, int np, const ulonglong2* tw_host, const ulonglong2* itw_host,
+                   long long n, std::vector<unsigned char>& B, std::vector<ulonglong2>& D);
 #endif
-int launch_ntt_col_tc(const NttArgs& a, int jobs, int batch, cudaStream_t st);
+int launch_ntt_col_tc(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st);
 
 // Fused row kernels (fused.cu)
 struct KsRowArgs {

@@ -214,7 +214,7 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
   count_launches((int)col + (int)row);
   const bool fp = a.ctw != nullptr;
   if (!inv) {
-    if (col && P1 == 8 && a.tcB && launch_ntt_col_tc(a, jobs, batch, st) == 0) {
+    if (col && P1 == 8 && a.tcB && launch_ntt_col_tc(a, jobs, batch, false, st) == 0) {
       // forward column phase ran on the tensor cores (ntt_tc.cu)
     } else if (col) {
       if (fp) ntt_col_kernel<P1, P2, false, true><<<gcol, bcol, 0, st>>>(a);
@@ -223,7 +223,9 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
     if (row) ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
   } else {
     if (row) ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
-    if (col) {
+    if (col && P1 == 8 && a.tcB && a.tc_inv && launch_ntt_col_tc(a, jobs, batch, true, st) == 0) {
+      // inverse column phase ran on the tensor cores (ntt_tc.cu)
+    } else if (col) {
       if (fp) ntt_col_kernel<P1, P2, true, true><<<gcol, bcol, 0, st>>>(a);
       else ntt_col_kernel<P1, P2, true, false><<<gcol, bcol, 0, st>>>(a);
     }

@@ -42,7 +42,8 @@ struct NttArgs {
   int logn;
   // tensor-core forward column phase (ntt_tc.cu; nullable: butterfly kernels)
   const unsigned char* tcB = nullptr;  // [prime][2][128 x 128 B] B1 | B2 in SMEM layout
-  const ulonglong2* tcD = nullptr;     // [prime][16][16] twists {d, d_shoup}
+  const ulonglong2* tcD = nullptr;     // [prime][2][16][16] twists {d, d_shoup}
+  int tc_inv = 1;                      // inverse column phase on the tensor cores too
 };
 
 // ---- compile-time pass schedule for a 2^P-point sub-transform ----

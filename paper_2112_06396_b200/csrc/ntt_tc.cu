@@ -115,17 +115,19 @@ __device__ __forceinline__ void st_u64(unsigned char* base, int row, int elem, u
 }
 
 // Tile t's 256 x 8 block goes straight from global memory into operand
-// layout with 8-byte cp.async (no registers): lane -> (c = lane & 7,
-// r_hi = 4 warp + lane / 8), iteration -> r_lo.  A warp's 32 copies land in
-// two 128-byte core-matrix rows (no bank conflicts) and read 4 x 64-byte
-// row segments.
-template <int P2>
+// layout with 8-byte cp.async (no registers).  Pass-1 operand row
+// (g1, c) = 8 g1 + c holds the 16 values of the contracted row bits e1:
+// forward g1 = r_lo, e1 = r_hi; inverse g1 = r_hi, e1 = r_lo.  Lane ->
+// (c = lane & 7, e1 = 4 (warp & 3) + lane / 8), iteration -> g1: a warp's 32
+// copies land in two 128-byte core-matrix rows (no bank conflicts).
+template <int P2, bool INV>
 __device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int c0, int gw, int lane) {
-  const int c = lane & 7, r_hi = 4 * (gw & 3) + (lane >> 3);   // gw: warp within the group
+  const int c = lane & 7, e1 = 4 * (gw & 3) + (lane >> 3);   // gw: warp within the group
 #pragma unroll
-  for (int r_lo = 8 * (gw >> 2); r_lo < 8 * (gw >> 2) + 8; ++r_lo) {
-    const u64* src = base + ((long long)(r_hi * 16 + r_lo) << P2) + c0 + c;
-    const unsigned dst = a_dst + kmaj_off(8 * r_lo + c, 8 * r_hi);
+  for (int g1 = 8 * (gw >> 2); g1 < 8 * (gw >> 2) + 8; ++g1) {
+    const int r = INV ? g1 * 16 + e1 : e1 * 16 + g1;
+    const u64* src = base + ((long long)r << P2) + c0 + c;
+    const unsigned dst = a_dst + kmaj_off(8 * g1 + c, 8 * e1);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -137,7 +139,7 @@ __device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int 
 // sharing the CTA's B matrices and twists.  Tile t+4's data streams in
 // (cp.async) while tile t is on the tensor cores and in the epilogues; the
 // two warps of a TMEM lane quarter split each epilogue's 16 outputs.
-template <int P2>
+template <int P2, bool INV>
 __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   unsigned char* Bm = tsm + 2 * kTcGroups * kOpBytes;      // A[group][2] (16 KB each), then B1 | B2
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   const int bar_id = 1 + grp;
   auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kTcGW) : "memory"); };
 
-  stage_tile<P2>(abuf_s, base, cbase + grp * kTcCols, gw, lane);      // this group's first tile
+  stage_tile<P2, INV>(abuf_s, base, cbase + grp * kTcCols, gw, lane);  // this group's first tile
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
         (unsigned)__cvta_generic_to_shared(tslot)), "n"(128 * kTcGroups));
@@ -170,12 +172,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   }
   if (gtid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s));
   {
-    const uint4* src = (const uint4*)(a.tcB + (size_t)prime * 2 * kBBytes);
+    const uint4* src = (const uint4*)(a.tcB + ((size_t)prime * 4 + (INV ? 2 : 0)) * kBBytes);
     uint4* dst = (uint4*)Bm;
     for (int i = tid; i < 2 * kBBytes / 16; i += kTcThreads) dst[i] = __ldg(src + i);
-    const ulonglong2* ts = a.tcD + (size_t)prime * 256;
+    const ulonglong2* ts = a.tcD + ((size_t)prime * 2 + (INV ? 1 : 0)) * 256;
     for (int i = tid; i < 256; i += kTcThreads) tw[i] = __ldg(ts + i);
   }
+  // inverse: the INTT's final scale n^-1 (times the optional extra constant)
+  const ulonglong2 scl = !INV ? make_ulonglong2(0, 0)
+                              : (a.scale ? a.scale[job] : make_ulonglong2(a.pc[prime].ninv, a.pc[prime].ninvp));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     gsync();
     tc_fence_after();
     if (tile + kTcGroups < kTcTiles)
-      stage_tile<P2>(abuf_s + ((it + 1) & 1) * kOpBytes, base, c0 + kTcGroups * kTcCols, gw, lane);
+      stage_tile<P2, INV>(abuf_s + ((it + 1) & 1) * kOpBytes, base, c0 + kTcGroups * kTcCols, gw, lane);
     // ---- pass 1: D1[(r_lo,c)][(beta,b)] = A1 . B1^T
     if (gtid == 0) {
 #pragma unroll
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     phase ^= 1;
     tc_fence_after();
     {
-      const int r_lo = m >> 3, c = m & 7;
+      const int g1 = m >> 3, c = m & 7;
 #pragma unroll 1
       for (int h = 2 * half; h < 2 * half + 2; ++h) {   // 4 outputs (32 TMEM columns) per wait
         uint32_t sv[32];
@@ -215,10 +220,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
         tmem_wait_ld();
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int beta = h * 4 + u;
+          const int o = h * 4 + u;                      // pass-1 output index
           const u64 y = reduce_lazy(sv + 8 * u, p, pinv32);
-          const ulonglong2 d = tw[beta * 16 + r_lo];
-          st_u64(A, beta * 8 + c, r_lo, shoup_lazy(y, d.x, d.y, p));  // [0, 2p)
+          const ulonglong2 d = tw[o * 16 + g1];
+          st_u64(A, o * 8 + c, g1, shoup_lazy(y, d.x, d.y, p));  // [0, 2p)
         }
       }
     }
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     phase ^= 1;
     tc_fence_after();
     {
-      const int beta = m >> 3, c = m & 7;
+      const int o1 = m >> 3, c = m & 7;
       u64* col = base + c0 + c;
 #pragma unroll 1
       for (int h = 2 * half; h < 2 * half + 2; ++h) {
@@ -246,8 +251,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
         tmem_ld32(tl + h * 32, sv);
         tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          col[(long long)(beta * 16 + h * 4 + u) << P2] = reduce_lazy(sv + 8 * u, p, pinv32);
+        for (int u = 0; u < 4; ++u) {
+          const int o2 = h * 4 + u;
+          const u64 v = reduce_lazy(sv + 8 * u, p, pinv32);
+          if (INV)  // rows 16 o2 + o1; canonical (the base conversion needs exact residues)
+            col[(long long)(o2 * 16 + o1) << P2] = shoup(v, scl.x, scl.y, p);
+          else      // rows 16 o1 + o2; lazy (0, 2p)
+            col[(long long)(o1 * 16 + o2) << P2] = v;
+        }
       }
     }
     tc_fence_before();   // the next tile's MMA rewrites D: TMEM reads are complete
@@ -261,16 +272,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
 
 constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 64;
 
-template <int P2>
+template <int P2, bool INV>
 int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ntt_col_tc_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(ntt_col_tc_kernel<P2, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kTcSmem);
     attr = true;
   }
   const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
-  ntt_col_tc_kernel<P2><<<grid, kTcThreads, kTcSmem, st>>>(a);
+  ntt_col_tc_kernel<P2, INV><<<grid, kTcThreads, kTcSmem, st>>>(a);
   return 0;
 }
 
@@ -301,61 +312,134 @@ void col_stages(std::vector<u64>& x, const ulonglong2* tw, u64 q, int s0, int s1
 
 }  // namespace
 
-bool ntt_tc_tables(const u64* mod, int np, const ulonglong2* tw_host, long long n,
-                   std::vector<unsigned char>& B, std::vector<ulonglong2>& D) {
-  B.assign((size_t)np * 2 * kBBytes, 0);
-  D.assign((size_t)np * 256, make_ulonglong2(0, 0));
+namespace {
+
+// Run GS stages s in [s0, s1) of the inverse 256-row column phase (rows at
+// distance t = 2^s, twiddle itw[128/2^s + block], rnspoly.py:64-79).
+void col_stages_inv(std::vector<u64>& x, const ulonglong2* itw, u64 q, int s0, int s1) {
+  for (int s = s0; s < s1; ++s) {
+    const int t = 1 << s, h = 128 >> s;
+    for (int blk = 0; blk < h; ++blk) {
+      const u64 w = itw[h + blk].x;
+      for (int j = blk * 2 * t; j < blk * 2 * t + t; ++j) {
+        const u64 u = x[j], v = x[j + t];
+        x[j] = (u + v) % q;
+        x[j + t] = mm((u + q - v) % q, w, q);
+      }
+    }
+  }
+}
+
+void put_b(unsigned char* dst, const u64 (&mat)[16][16], u64 q) {
+  // B[n = 8k + b][byte 8j + a] = byte b of (Mat[k][j] 2^8a mod q)
+  for (int k = 0; k < 16; ++k)
+    for (int j = 0; j < 16; ++j) {
+      u64 v = mat[k][j];
+      for (int aa = 0; aa < 8; ++aa) {
+        for (int b = 0; b < 8; ++b) dst[kmaj_off(8 * k + b, 8 * j + aa)] = (unsigned char)(v >> (8 * b));
+        v = mm(v, 256 % q, q);
+      }
+    }
+}
+
+ulonglong2 shp(u64 d, u64 q) { return make_ulonglong2(d, (u64)(((u128)d << 64) / q)); }
+
+// Forward: M1 on r_hi (shared), then block beta = r_hi: M2[beta] = F diag(d_beta).
+bool fwd_tables(u64 q, const ulonglong2* tw, unsigned char* B, ulonglong2* D) {
+  u64 M1[16][16], M2[16][16][16];  // M2[beta][k][j]
+  for (int j = 0; j < 16; ++j) {
+    std::vector<u64> x(256, 0);
+    x[16 * j] = 1;
+    col_stages(x, tw, q, 0, 4);
+    for (int k = 0; k < 16; ++k) M1[k][j] = x[16 * k];
+    for (int beta = 0; beta < 16; ++beta) {
+      std::vector<u64> y(256, 0);
+      y[16 * beta + j] = 1;
+      col_stages(y, tw, q, 4, 8);
+      for (int k = 0; k < 16; ++k) M2[beta][k][j] = y[16 * beta + k];
+      for (int r = 0; r < 256; ++r)
+        if ((r >> 4) != beta && y[r]) return false;  // M2 must not leak across blocks
+    }
+  }
+  for (int beta = 0; beta < 16; ++beta)
+    for (int j = 0; j < 16; ++j) {
+      if (M2[0][0][j] == 0) return false;
+      const u64 d = mm(M2[beta][0][j], pw(M2[0][0][j], q - 2, q), q);
+      for (int k = 0; k < 16; ++k)
+        if (mm(M2[0][k][j], d, q) != M2[beta][k][j]) return false;
+      D[beta * 16 + j] = shp(d, q);  // indexed [pass-1 output beta][pass-1 row bits r_lo]
+    }
+  put_b(B, M1, q);
+  put_b(B + kBBytes, M2[0], q);
+  return true;
+}
+
+// Inverse: block beta = r_hi first, M1[beta] = diag(e_beta) G on r_lo (output
+// twist), then M2 on r_hi (shared).
+bool inv_tables(u64 q, const ulonglong2* itw, unsigned char* B, ulonglong2* D) {
+  u64 M1[16][16][16], M2[16][16];  // M1[beta][k][j]
+  for (int j = 0; j < 16; ++j) {
+    for (int beta = 0; beta < 16; ++beta) {
+      std::vector<u64> y(256, 0);
+      y[16 * beta + j] = 1;
+      col_stages_inv(y, itw, q, 0, 4);
+      for (int k = 0; k < 16; ++k) M1[beta][k][j] = y[16 * beta + k];
+      for (int r = 0; r < 256; ++r)
+        if ((r >> 4) != beta && y[r]) return false;
+    }
+    for (int r_lo : {0, 5}) {  // M2 must be the same for every r_lo
+      std::vector<u64> x(256, 0);
+      x[16 * j + r_lo] = 1;
+      col_stages_inv(x, itw, q, 4, 8);
+      for (int k = 0; k < 16; ++k) {
+        if (r_lo == 0) M2[k][j] = x[16 * k];
+        else if (x[16 * k + r_lo] != M2[k][j]) return false;
+      }
+    }
+  }
+  for (int beta = 0; beta < 16; ++beta)
+    for (int k = 0; k < 16; ++k) {
+      if (M1[0][k][0] == 0) return false;
+      const u64 e = mm(M1[beta][k][0], pw(M1[0][k][0], q - 2, q), q);
+      for (int j = 0; j < 16; ++j)
+        if (mm(M1[0][k][j], e, q) != M1[beta][k][j]) return false;
+      D[k * 16 + beta] = shp(e, q);  // indexed [pass-1 output k][pass-1 row bits beta]
+    }
+  put_b(B, M1[0], q);
+  put_b(B + kBBytes, M2, q);
+  return true;
+}
+
+}  // namespace
+
+// Per plan prime: B = [fwd B1 | fwd B2 | inv B1 | inv B2] (4 x 16 KB, SMEM layout),
+// D = [fwd twists | inv twists] (2 x 256 {d, d_shoup}).  False if any prime
+// is too small for reduce_lazy or a factorisation check fails.
+bool ntt_tc_tables(const u64* mod, int np, const ulonglong2* tw_host, const ulonglong2* itw_host,
+                   long long n, std::vector<unsigned char>& B, std::vector<ulonglong2>& D) {
+  B.assign((size_t)np * 4 * kBBytes, 0);
+  D.assign((size_t)np * 512, make_ulonglong2(0, 0));
   for (int pi = 0; pi < np; ++pi) {
     const u64 q = mod[pi];
     if ((double)q < 796131459065721.0) return false;  // reduce_lazy needs p > 2^49.5
-    const ulonglong2* tw = tw_host + (size_t)pi * n;
-    u64 M1[16][16], M2[16][16][16];  // M2[beta][k][j]
-    for (int j = 0; j < 16; ++j) {
-      std::vector<u64> x(256, 0);
-      x[16 * j] = 1;
-      col_stages(x, tw, q, 0, 4);
-      for (int k = 0; k < 16; ++k) M1[k][j] = x[16 * k];
-      for (int beta = 0; beta < 16; ++beta) {
-        std::vector<u64> y(256, 0);
-        y[16 * beta + j] = 1;
-        col_stages(y, tw, q, 4, 8);
-        for (int k = 0; k < 16; ++k) M2[beta][k][j] = y[16 * beta + k];
-        // M1 must not leak across r_lo, nor M2 across blocks
-        for (int r = 0; r < 256; ++r)
-          if ((r >> 4) != beta && y[r]) return false;
-      }
-    }
-    // F = M2[0]; twist d_beta[j] = M2[beta][0][j] / F[0][j]; verify M2[beta] = F diag(d_beta)
-    for (int beta = 0; beta < 16; ++beta)
-      for (int j = 0; j < 16; ++j) {
-        if (M2[0][0][j] == 0) return false;
-        const u64 d = mm(M2[beta][0][j], pw(M2[0][0][j], q - 2, q), q);
-        for (int k = 0; k < 16; ++k)
-          if (mm(M2[0][k][j], d, q) != M2[beta][k][j]) return false;
-        D[(size_t)pi * 256 + beta * 16 + j] = make_ulonglong2(d, (u64)(((u128)d << 64) / q));
-      }
-    // B matrices: B[n = 8k + b][byte 8j + a] = byte b of (Mat[k][j] 2^8a mod q)
-    for (int which = 0; which < 2; ++which) {
-      unsigned char* dst = B.data() + ((size_t)pi * 2 + which) * kBBytes;
-      for (int k = 0; k < 16; ++k)
-        for (int j = 0; j < 16; ++j) {
-          u64 v = which == 0 ? M1[k][j] : M2[0][k][j];
-          for (int aa = 0; aa < 8; ++aa) {
-            for (int b = 0; b < 8; ++b) dst[kmaj_off(8 * k + b, 8 * j + aa)] = (unsigned char)(v >> (8 * b));
-            v = mm(v, 256 % q, q);
-          }
-        }
-    }
+    if (!fwd_tables(q, tw_host + (size_t)pi * n, B.data() + (size_t)pi * 4 * kBBytes,
+                    D.data() + (size_t)pi * 512))
+      return false;
+    if (!inv_tables(q, itw_host + (size_t)pi * n, B.data() + ((size_t)pi * 4 + 2) * kBBytes,
+                    D.data() + (size_t)pi * 512 + 256))
+      return false;
   }
   return true;
 }
 
-// Forward column phase on the tensor cores (P1 = 8 only); -1 if not applicable.
-int launch_ntt_col_tc(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
+// Column phase on the tensor cores (P1 = 8 only); -1 if not applicable.
+int launch_ntt_col_tc(const NttArgs& a, int jobs, int batch, bool inverse, cudaStream_t st) {
   if (!a.tcB || !a.tcD) return -1;
-  switch (a.logn) {
-    case 16: return launch_t<8>(a, jobs, batch, st);
-    case 17: return launch_t<9>(a, jobs, batch, st);
+  switch (a.logn * 2 + (int)inverse) {
+    case 32: return launch_t<8, false>(a, jobs, batch, st);
+    case 33: return launch_t<8, true>(a, jobs, batch, st);
+    case 34: return launch_t<9, false>(a, jobs, batch, st);
+    case 35: return launch_t<9, true>(a, jobs, batch, st);
     default: return -1;
   }
 }
