@@ -12,54 +12,76 @@
 
 namespace ck {
 
-constexpr int kDiagThreads = 256;
+// threads per CTA: the baby inputs (2 x MB u64 per thread) fit 32 KB of static SMEM
+template <int MB>
+constexpr int diag_threads() { return MB <= 16 ? 128 : 64; }
 constexpr int kMaxBaby = 32;
 
 // MB: compile-time upper bound on the baby count (fully unrolled, baby
-// inputs stay in registers; entries k >= baby are never touched).
+// inputs stay in registers; entries k >= baby are never touched).  A thread
+// owns one coefficient of one raised row for BOTH u and v, so every diagonal
+// element is loaded once and feeds two accumulators.
 template <int MB>
-__global__ void __launch_bounds__(kDiagThreads) diag_mac_kernel(DiagArgs a) {
+__global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArgs a) {
+  constexpr int NT = diag_threads<MB>();
+  // baby inputs of this thread's coefficient, u then v (thread-private columns:
+  // shared memory only keeps them out of the register file)
+  __shared__ u64 xs[2 * MB][NT];
   const int n = 1 << a.logn;
-  const int c = blockIdx.x * kDiagThreads + threadIdx.x;
+  const int c = blockIdx.x * NT + threadIdx.x;
   const int i = blockIdx.y;
-  const int w = blockIdx.z;  // 0: u, 1: v
   if (c >= n) return;
+  const int t = threadIdx.x;
   const PrimeConst& P = a.pc[a.prime[i]];
   const long long rowN = (long long)a.R << a.logn;
-  u64 x[MB];
+  const long long off = ((long long)i << a.logn) + c;
 #pragma unroll
   for (int k = 0; k < MB; ++k) {
-    x[k] = 0;
     if (k < a.baby) {
-      u64 v = a.uv[(2LL * k + w) * rowN + ((long long)i << a.logn) + c];
-      if (w == 1 && i < a.l) {
-        const u64 t = a.galois[k];
-        const u64 bv = a.b[((long long)i << a.logn) + automorph_src((u32)c, (u32)t, a.logn)];
+      xs[2 * k][t] = a.uv[(2LL * k) * rowN + off];
+      u64 v = a.uv[(2LL * k + 1) * rowN + off];
+      if (i < a.l) {
+        const u64 g = a.galois[k];
+        const u64 bv = a.b[((long long)i << a.logn) + automorph_src((u32)c, (u32)g, a.logn)];
         const ulonglong2 pm = a.pmod[i];
         v = addmod(v, shoup(bv, pm.x, pm.y, P.q), P.q);
       }
-      x[k] = v;
+      xs[2 * k + 1][t] = v;
     }
   }
   for (int j = 0; j < a.giant; ++j) {
-    const u64* d = a.diags + (long long)j * a.baby * rowN + ((long long)i << a.logn) + c;
-    u64 y = 0;
+    const u64* d = a.diags + (long long)j * a.baby * rowN + off;
+    u64 yu = 0, yv = 0;
+    // every diagonal of this giant group is requested before the first MAC
+    constexpr int KL = MB < 16 ? MB : 16;
 #pragma unroll
-    for (int k0 = 0; k0 < MB; k0 += 8) {
+    for (int k1 = 0; k1 < MB; k1 += KL) {
+    if (k1 >= a.baby) continue;
+    u64 m[KL];
+#pragma unroll
+    for (int kk = 0; kk < KL; ++kk) m[kk] = k1 + kk < a.baby ? __ldg(d + (k1 + kk) * rowN) : 0;
+#pragma unroll
+    for (int k0 = k1; k0 < k1 + KL; k0 += 8) {
       if (k0 >= a.baby) continue;
-      Acc3 s;
-      acc3_zero(s);
+      Acc3 su, sv;
+      acc3_zero(su);
+      acc3_zero(sv);
 #pragma unroll
       for (int kk = 0; kk < 8 && k0 + kk < MB; ++kk) {
         const int k = k0 + kk;
         if (k < a.baby) {
-          const u64 m = __ldg(d + k * rowN);
-          acc3_mac(s, lo30(m), hi30(m), lo30(x[k]), hi30(x[k]));
+          const u32 m0 = lo30(m[k - k1]), m1 = hi30(m[k - k1]);
+          const u64 xu = xs[2 * k][t], xv = xs[2 * k + 1][t];
+          acc3_mac(su, m0, m1, lo30(xu), hi30(xu));
+          acc3_mac(sv, m0, m1, lo30(xv), hi30(xv));
         }
       }
-      y = addmod(y, acc3_reduce(s, P), P.q);
+      yu = addmod(yu, acc3_reduce(su, P), P.q);
+      yv = addmod(yv, acc3_reduce(sv, P), P.q);
     }
-    a.acc[(2LL * j + w) * rowN + ((long long)i << a.logn) + c] = y;
+    }
+    a.acc[(2LL * j) * rowN + off] = yu;
+    a.acc[(2LL * j + 1) * rowN + off] = yv;
   }
 }
 
@@ -67,11 +89,14 @@ int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
   if (a.baby < 1 || a.baby > kMaxBaby || a.giant < 1) return CK_ERR_ARG;
   count_launches(1);
   const int n = 1 << a.logn;
-  const dim3 grid((n + kDiagThreads - 1) / kDiagThreads, a.R, 2);
-  if (a.baby <= 4) diag_mac_kernel<4><<<grid, kDiagThreads, 0, st>>>(a);
-  else if (a.baby <= 8) diag_mac_kernel<8><<<grid, kDiagThreads, 0, st>>>(a);
-  else if (a.baby <= 16) diag_mac_kernel<16><<<grid, kDiagThreads, 0, st>>>(a);
-  else diag_mac_kernel<32><<<grid, kDiagThreads, 0, st>>>(a);
+#define CK_DIAG(MB)                                                                    \
+  diag_mac_kernel<MB><<<dim3((n + diag_threads<MB>() - 1) / diag_threads<MB>(), a.R),       \
+                        diag_threads<MB>(), 0, st>>>(a)
+  if (a.baby <= 4) CK_DIAG(4);
+  else if (a.baby <= 8) CK_DIAG(8);
+  else if (a.baby <= 16) CK_DIAG(16);
+  else CK_DIAG(32);
+#undef CK_DIAG
   return (int)cudaGetLastError();
 }
 

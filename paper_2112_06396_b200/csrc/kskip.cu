@@ -21,8 +21,11 @@ CK_HD int ks_row_bits(int logn) { return logn < 9 ? logn : 9; }
 constexpr int kKsThreads = 256;
 constexpr int kKsMaxBeta = 8;
 
-// grid = (N / TILE, rows, batch); TILE = 512 elements (or N if smaller)
-template <int TILE>
+// grid = (N / TILE, rows, batch); TILE = 512 elements (or N if smaller).
+// BETA > 0: compile-time digit count, every key element of a thread's
+// coefficients is requested before the first multiply (the kernel streams
+// keys, so memory-level parallelism is what matters); BETA = 0: runtime.
+template <int TILE, int BETA = 0>
 __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
   __shared__ u64 sd[kKsMaxBeta][TILE];
   const int logn = a.logn;
@@ -34,6 +37,9 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
   const PrimeConst P = a.pc[prime];
   const u64 t = a.galois ? a.galois[bz] : a.galois_t;
   const long long tile0 = (long long)blockIdx.x * TILE;
+  const int krow = a.key_row[i];
+  const u64* kb = a.key_b + bz * a.key_batch + ((long long)krow << logn);
+  const u64* ka = a.key_a + bz * a.key_batch + ((long long)krow << logn);
   const u64* dig = a.digits + bz * a.digits_batch + ((long long)i << logn);
   // stage the gathered digit rows: for each storage row in the tile load the
   // source row perm maps it to
@@ -49,11 +55,43 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
     }
   }
   __syncthreads();
-  const int krow = a.key_row[i];
-  const u64* kb = a.key_b + bz * a.key_batch + ((long long)krow << logn);
-  const u64* ka = a.key_a + bz * a.key_batch + ((long long)krow << logn);
   u64* uo = a.u + bz * a.out_batch + ((long long)i << logn);
   u64* vo = a.v + bz * a.out_batch + ((long long)i << logn);
+  if constexpr (BETA > 0) {
+    constexpr int PER = TILE / kKsThreads;  // coefficients per thread
+    u64 ya[PER][BETA], yb[PER][BETA];
+#pragma unroll
+    for (int h = 0; h < PER; ++h)
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        const long long o = tile0 + threadIdx.x + h * kKsThreads;
+        ya[h][d] = __ldg(ka + d * a.key_digit_stride + o);
+        yb[h][d] = __ldg(kb + d * a.key_digit_stride + o);
+      }
+#pragma unroll
+    for (int h = 0; h < PER; ++h) {
+      const int e = threadIdx.x + h * kKsThreads;
+      const long long o = tile0 + e;
+      int se = e;
+      if (t != 1) {
+        const u32 src = automorph_src((u32)o, (u32)t, logn);
+        se = (int)((o & ~(long long)(rowlen - 1)) - tile0) + (int)(src & (rowlen - 1));
+      }
+      Acc3 su, sv;
+      acc3_zero(su);
+      acc3_zero(sv);
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        const u64 x = sd[d][se];
+        const u32 x0 = lo30(x), x1 = hi30(x);
+        acc3_mac(su, x0, x1, lo30(ya[h][d]), hi30(ya[h][d]));
+        acc3_mac(sv, x0, x1, lo30(yb[h][d]), hi30(yb[h][d]));
+      }
+      uo[o] = acc3_reduce(su, P);
+      vo[o] = acc3_reduce(sv, P);
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
     const long long o = tile0 + e;
     int se = e;
@@ -83,7 +121,10 @@ int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st) {
   const int n = 1 << a.logn;
   count_launches(1);
   if (n >= 512) {
-    kskip_kernel<512><<<dim3(n / 512, rows, batch), kKsThreads, 0, st>>>(a);
+    const dim3 g(n / 512, rows, batch);
+    if (a.beta == 3) kskip_kernel<512, 3><<<g, kKsThreads, 0, st>>>(a);
+    else if (a.beta == 4) kskip_kernel<512, 4><<<g, kKsThreads, 0, st>>>(a);
+    else kskip_kernel<512><<<g, kKsThreads, 0, st>>>(a);
   } else {
     // small rings: one tile holds the whole limb (row_bits == logn)
     switch (a.logn) {
