@@ -1257,15 +1257,31 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint
     return ew_run(p, ck::EW_COPY, out_b, 0, rb, 0, nullptr, 0, nullptr, 0, kp, nullptr, 1, nullptr,
                   (int)lo, 1, st);
   }
-  CK_TRY(ew_run(p, ck::EW_ADD, out_a, 0, ra, 0, ra + lo * N, 0, nullptr, 0, kp, nullptr, 1,
-                nullptr, (int)lo, 1, st));
-  CK_TRY(ew_run(p, ck::EW_ADD, out_b, 0, rb, 0, rb + lo * N, 0, nullptr, 0, kp, nullptr, 1,
-                nullptr, (int)lo, 1, st));
-  for (int j = 2; j < giant; ++j) {
-    CK_TRY(ew_run(p, ck::EW_ADD, out_a, 0, out_a, 0, ra + j * lo * N, 0, nullptr, 0, kp, nullptr,
-                  1, nullptr, (int)lo, 1, st));
-    CK_TRY(ew_run(p, ck::EW_ADD, out_b, 0, out_b, 0, rb + j * lo * N, 0, nullptr, 0, kp, nullptr,
-                  1, nullptr, (int)lo, 1, st));
+  // one pass over all giants per output (instead of giant - 1 pairwise adds)
+  for (int half = 0; half < 2; ++half) {
+    const u64* src = half ? rb : ra;
+    u64* dst = half ? out_b : out_a;
+    for (int j0 = 0; j0 < giant; j0 += 16) {
+      const int cnt = std::min(16, giant - j0);
+      ck::EwArgs e{};
+      e.out = dst;
+      e.x = j0 ? dst : src;
+      e.y = nullptr;
+      e.y_batch = lo * N;
+      e.prime = kp;
+      e.pc = p->d_pc;
+      e.galois_t = 1;
+      e.op = ck::EW_SUMN;
+      e.logn = p->logn;
+      e.count = cnt;
+      if (j0) {  // running total + the next chunk: fold the chunk into dst pairwise
+        for (int j = j0; j < j0 + cnt; ++j)
+          CK_TRY(ew_run(p, ck::EW_ADD, dst, 0, dst, 0, src + j * lo * N, 0, nullptr, 0, kp, nullptr,
+                        1, nullptr, (int)lo, 1, st));
+        continue;
+      }
+      CK_TRY(ck::launch_ew(e, (int)lo, 1, st));
+    }
   }
   return 0;
 }

@@ -158,7 +158,7 @@ int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st);
 
 // Elementwise ops over limb rows.
 enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_MULC = 4, EW_COPY = 5,
-            EW_MODDOWN = 6, EW_AUTOMORPH = 7 };
+            EW_MODDOWN = 6, EW_AUTOMORPH = 7, EW_SUMN = 8 };
 struct EwArgs {
   u64* out;
   const u64* x;
@@ -171,6 +171,7 @@ struct EwArgs {
   u64 galois_t;                 // AUTOMORPH / MODDOWN addend gather (1 = none)
   const u64* galois;            // per batch item (nullable: galois_t)
   int op, logn;
+  int count = 0;                // SUMN: out = sum_{j < count} x[j * y_batch] (count <= 16)
 };
 int launch_ew(const EwArgs& a, int rows, int batch, cudaStream_t st);
 
