@@ -285,18 +285,31 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---- end to end through the public API with host buffers
     e2e = None
+    ok, why = 1.0, "pinned host buffers could not be allocated on every rank"
     if not args.no_e2e:
-        from paper_2112_06396_b200.ckks import HostRotationPipeline
         ins = [wb.a, wb.b, wb.key_b, wb.key_a]
         # pinned host buffers filled straight from the device (no pageable copy:
         # at N=8 every rank holds ~10 GB of inputs)
-        host_in = []
-        for t in ins:
-            h = torch.empty(t.shape, dtype=torch.uint64, pin_memory=True)
-            h.copy_(t)
-            host_in.append(h)
-        host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
+        host_in, host_out = [], []
+        try:
+            for t in ins:
+                h = torch.empty(t.shape, dtype=torch.uint64, pin_memory=True)
+                h.copy_(t)
+                host_in.append(h)
+            host_out = [torch.empty(wb.out_a.shape, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
+        except RuntimeError as exc:  # e.g. pinned host memory exhausted with many ranks
+            ok, why = 0.0, "pinned host buffers: " + str(exc).splitlines()[0][:160]
+        # every rank must agree before the (barrier-synchronised) e2e run
+        if world > 1:
+            flag = torch.tensor([ok], dtype=torch.float64, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = float(flag.item())
         del ins
+    if not args.no_e2e and ok == 0.0:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "unavailable": why}
+    elif not args.no_e2e:
+        from paper_2112_06396_b200.ckks import HostRotationPipeline
         wb.release_inputs()  # the host pipeline owns its own device buffers
         pipe = HostRotationPipeline(p, B, chunk=args.e2e_chunk, nbuf=args.e2e_nbuf)
         ke = max(1, min(args.steps, args.e2e_steps))

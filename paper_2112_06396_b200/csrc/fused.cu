@@ -30,7 +30,13 @@ struct FusedCfg {
   static constexpr int NT = TR * G;        // EPC / 16 threads
   static constexpr int RS = row_stride<P2>();
 };
-constexpr int kKsEpc = 2048;  // ks_row: small CTAs -> 8 resident per SM (phase diversity)
+#ifndef CKB200_KS_EPC
+#define CKB200_KS_EPC 2048
+#endif
+#ifndef CKB200_KS_MINB
+#define CKB200_KS_MINB 4
+#endif
+constexpr int kKsEpc = CKB200_KS_EPC;  // ks_row elements per CTA (2048: 128 threads, 4 CTAs/SM)
 
 // ---------------------------------------------------------------- KSKIP row
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
@@ -42,7 +48,7 @@ constexpr int kKsEpc = 2048;  // ks_row: small CTAs -> 8 resident per SM (phase 
 // automorphism gather happens at MAC time (one permutation index per element,
 // shared by all digits) -- no separate staging buffer.
 template <int P1, int P2, int BETA>
-__global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, 4) ks_row_kernel(KsRowArgs a) {
+__global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_row_kernel(KsRowArgs a) {
   using F = FusedCfg<P2, kKsEpc>;
   constexpr int LOGN = P1 + P2;
   constexpr int SLOT = F::TR * F::RS;
