@@ -38,6 +38,34 @@ struct FusedCfg {
 #endif
 constexpr int kKsEpc = CKB200_KS_EPC;  // ks_row elements per CTA (2048: 128 threads, 4 CTAs/SM)
 
+// Forward row phase of one digit tile in shared memory (natural order in and
+// out).  Not inlined (CKB200_KS_NOINLINE, default 1): ONE copy of this code per kernel instead
+// of one per digit: ks_row_kernel<8,8,3> is ~140 KB of SASS, above the SM's
+// instruction cache (no_instruction stalls; measured +1.3% with the call).
+#ifndef CKB200_KS_NOINLINE
+#define CKB200_KS_NOINLINE 1
+#endif
+#if CKB200_KS_NOINLINE
+#define CK_KS_DIGIT_INLINE __noinline__
+#else
+#define CK_KS_DIGIT_INLINE __forceinline__
+#endif
+template <int P2, int LOGN>
+__device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const ulonglong2* tw,
+                                                u64 q, u64 two_q) {
+  u64 x[kE];
+  row_from_smem<P2, 0, false>(x, g, srow);
+  row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
+  // the 30-bit-split MAC only needs digits < 2^60: for q < 2^56 the lazy
+  // range [0, 16q) already is; larger (special) primes are reduced
+  if (q >= (1ull << 56)) {
+#pragma unroll
+    for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+  }
+  __syncthreads();
+  row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+}
+
 // ---------------------------------------------------------------- KSKIP row
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
 // 2*BETA key loads of an element are independent and stay in flight);
@@ -104,19 +132,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       else if (d == 1) cp_async_wait<(BETA >= 2 ? BETA - 2 : 0)>();
       else if (d == 2) cp_async_wait<(BETA >= 3 ? BETA - 3 : 0)>();
       else cp_async_wait<0>();
-      if (!own) {  // own rows are already in place (natural order)
-        u64 x[kE];
-        row_from_smem<P2, 0, false>(x, g, srow);
-        row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
-        // the 30-bit-split MAC only needs digits < 2^60: for q < 2^56 the lazy
-        // range [0, 16q) already is; larger (special) primes are reduced
-        if (q >= (1ull << 56)) {
-#pragma unroll
-          for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
-        }
-        __syncthreads();
-        row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
-      }
+      if (!own) ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);  // own rows are in place
     }
   } else {
 #pragma unroll 1
