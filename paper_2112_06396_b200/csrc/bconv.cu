@@ -162,7 +162,7 @@ constexpr int kTcRows = kTcWarps * 32;  // coefficients per tile (2 m16 blocks p
 constexpr int kTcXs = kTcRows + 8;      // padded u64 row stride of the staged sources
 constexpr int kTcTiles = 4;             // row tiles per CTA
 #ifndef CKB200_BCTC_MINB
-#define CKB200_BCTC_MINB 4                // resident CTAs per SM the registers are sized for
+#define CKB200_BCTC_MINB 6                // resident CTAs per SM the registers are sized for (4: -1.2%)
 #endif
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) {
