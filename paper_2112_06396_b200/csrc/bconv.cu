@@ -209,6 +209,7 @@ __device__ __forceinline__ void tc_stage(u64* xs, const BconvArgs& a, const u64*
 
 template <int KS>
 __global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kernel(const __grid_constant__ BconvGroups G) {
+  pdl_trigger();
   const BconvArgs& a = G.g[blockIdx.y];
   extern __shared__ __align__(16) unsigned char tc_smem[];
   const int nd = a.nd, ns = a.ns;
@@ -232,8 +233,6 @@ __global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kern
     const int b = e / ((4 * KS - ns) * kTcXs), rem = e - b * ((4 * KS - ns) * kTcXs);
     xsb[b * 4 * KS * kTcXs + ns * kTcXs + rem] = 0;
   }
-  tc_stage<KS>(xsb, a, in, t0 * kTcRows, n);
-  cp_async_commit();
   for (int i = tid; i < tks * ntile * 32; i += blockDim.x) bf[i] = a.Bf[i];
   for (int j = tid; j < nd; j += blockDim.x) {
     const u64 p = a.pc[a.dst_prime[j]].q;
@@ -241,6 +240,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kern
   }
   if (a.centered)
     for (int i = tid; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
+  pdl_wait();  // the sources are the predecessor's output
+  tc_stage<KS>(xsb, a, in, t0 * kTcRows, n);
+  cp_async_commit();
 
   const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
   u64* out = a.out + (long long)blockIdx.z * a.out_batch;
@@ -351,7 +353,7 @@ static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
   }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(bconv_tc_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  bconv_tc_kernel<KS><<<grid, kTcWarps * 32, smem, st>>>(G);
+  launch_pdl(bconv_tc_kernel<KS>, grid, dim3(kTcWarps * 32), smem, st, G);
 }
 
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st) {

@@ -28,6 +28,13 @@ typedef unsigned __int128 u128;
 static std::atomic<long long> g_launches{0};
 namespace ck {
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CKB200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 }  // namespace ck
 
 namespace {

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   constexpr int LOGN = P1 + P2;
   constexpr int SLOT = F::TR * F::RS;
   extern __shared__ __align__(16) u64 fsm[];
+  pdl_trigger();
   const int i = blockIdx.z;            // grid (row tile, batch, limb): see ks_row_ws_kernel
   const long long b = blockIdx.y;
   const int prime = a.prime[i];
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
                     ((long long)blockIdx.x * F::TR << P2),
                 (F::TR * F::S * 8 / 8) * min(a.key_prefetch, 8));
   }
+  pdl_wait();  // digits and the ciphertext rows are the predecessors' output
   if constexpr (BETA > 0) {
     // All digits' source rows are requested up front with async copies into
     // their own slots (natural order), so the loads of digits 1.. overlap the
@@ -446,6 +448,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   u64* srow = stage + rl * F::RS;
   const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
   const long long ro = ((long long)j << LOGN) + ((long long)r << P2);
+  pdl_trigger();
+  pdl_wait();
   const u64* conv = a.conv + b * a.conv_batch + ro + (a.pair && w ? a.conv_w : 0);
   const u64* x = a.x + b * a.x_batch + ro + (a.pair && w ? a.x_w : 0);
   u64 y[kE];
@@ -528,7 +532,7 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
                             : ks_row_kernel<P1, P2, 0>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<dim3((1 << P1) / F::TR, batch, rows), F::NT, smem, st>>>(a);
+  launch_pdl(kern, dim3((1 << P1) / F::TR, batch, rows), dim3(F::NT), smem, st, a);
   return 0;
 }
 
@@ -536,8 +540,8 @@ template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
   const dim3 grid((1 << P1) / F::TR, batch * (a.pair ? 2 : 1), rows);
-  if (a.lazy) md_row_kernel<P1, P2, true><<<grid, F::NT, 0, st>>>(a);
-  else md_row_kernel<P1, P2, false><<<grid, F::NT, 0, st>>>(a);
+  if (a.lazy) launch_pdl(md_row_kernel<P1, P2, true>, grid, dim3(F::NT), 0, st, a);
+  else launch_pdl(md_row_kernel<P1, P2, false>, grid, dim3(F::NT), 0, st, a);
   return 0;
 }
 

@@ -93,10 +93,12 @@ ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;
   __shared__ u64 sm[R::TR * R::RS];
+  pdl_trigger();
   const int job = blockIdx.z;  // grid (row tile, batch, job): twiddle reuse across the batch
   const int prime = a.prime_idx[job];
   const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
   const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
+  pdl_wait();
   u64* base = a.data + job_offset(a, job, blockIdx.y);
   const u64* ibase = a.src ? a.src + ((long long)job << a.logn) + (long long)blockIdx.y * a.src_batch_stride
                            : base;  // out-of-place input (e.g. ModUp reads the ciphertext directly)
@@ -220,9 +222,9 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
       if (fp) ntt_col_kernel<P1, P2, false, true><<<gcol, bcol, 0, st>>>(a);
       else ntt_col_kernel<P1, P2, false, false><<<gcol, bcol, 0, st>>>(a);
     }
-    if (row) ntt_row_kernel<P1, P2, false><<<grow, brow, 0, st>>>(a);
+    if (row) launch_pdl(ntt_row_kernel<P1, P2, false>, grow, brow, 0, st, a);
   } else {
-    if (row) ntt_row_kernel<P1, P2, true><<<grow, brow, 0, st>>>(a);
+    if (row) launch_pdl(ntt_row_kernel<P1, P2, true>, grow, brow, 0, st, a);
     if (col && P1 == 8 && a.tcB && a.tc_inv && launch_ntt_col_tc(a, jobs, batch, true, st) == 0) {
       // inverse column phase ran on the tensor cores (ntt_tc.cu)
     } else if (col) {

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   const int bar_id = 1 + grp;
   auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kTcGW) : "memory"); };
 
-  stage_tile<P2, INV>(abuf_s, base, cbase + grp * kTcCols, gw, lane);  // this group's first tile
+  pdl_trigger();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
         (unsigned)__cvta_generic_to_shared(tslot)), "n"(128 * kTcGroups));
@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     const ulonglong2* ts = a.tcD + ((size_t)prime * 2 + (INV ? 1 : 0)) * 256;
     for (int i = tid; i < 256; i += kTcThreads) tw[i] = __ldg(ts + i);
   }
+  pdl_wait();  // the predecessor's output is read from here on
+  stage_tile<P2, INV>(abuf_s, base, cbase + grp * kTcCols, gw, lane);  // this group's first tile
   // inverse: the INTT's final scale n^-1 (times the optional extra constant)
   const ulonglong2 scl = !INV ? make_ulonglong2(0, 0)
                               : (a.scale ? a.scale[job] : make_ulonglong2(a.pc[prime].ninv, a.pc[prime].ninvp));
@@ -281,7 +283,7 @@ int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
     attr = true;
   }
   const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
-  ntt_col_tc_kernel<P2, INV><<<grid, kTcThreads, kTcSmem, st>>>(a);
+  launch_pdl(ntt_col_tc_kernel<P2, INV>, grid, dim3(kTcThreads), kTcSmem, st, a);
   return 0;
 }
 
