@@ -5,7 +5,8 @@ also with FP64-assisted twiddles, CKB200_FPNTT=1); and the opt-in pipeline
 variants kept for measurement: unfused key-switch (CKB200_UNFUSED=1),
 warp-specialised ks_row (CKB200_KSWS=1), special-row INTT inside ks_row
 (CKB200_KSINTT=1), BC fused with the column phase (CKB200_BCCOL=1), CUDA-core
-BC (CKB200_BCTC=0), chunked multi-stream batches (CKB200_CHUNK/STREAMS).
+BC (CKB200_BCTC=0), chunked multi-stream batches (CKB200_CHUNK/STREAMS),
+plain launches instead of programmatic dependent launch (CKB200_PDL=0).
 Variants are read at plan creation, so each runs in a fresh process."""
 
 import os
@@ -44,6 +45,7 @@ VARIANTS = {
     "bc_fused_with_column_phase": {"CKB200_BCCOL": "1", "CKB200_NTTTC": "0"},
     "bc_cuda_cores": {"CKB200_BCTC": "0"},
     "chunked_two_streams": {"CKB200_CHUNK": "16", "CKB200_STREAMS": "2"},
+    "no_programmatic_dependent_launch": {"CKB200_PDL": "0"},
 }
 
 
