@@ -32,8 +32,12 @@ __host__ __device__ __forceinline__ u64 rotl64(u64 x, int n) {
 
 // The permutation: 24 rounds of theta, rho+pi, chi, iota; the whole state
 // stays in registers (all lane indices are compile-time constants).
+#ifndef CKB200_KECCAK_UNROLL
+#define CKB200_KECCAK_UNROLL 1
+#endif
+constexpr int kKeccakUnroll = CKB200_KECCAK_UNROLL;
 __host__ __device__ __forceinline__ void keccak_f1600(u64 (&s)[25]) {
-#pragma unroll 1
+#pragma unroll kKeccakUnroll
   for (int r = 0; r < 24; ++r) {
     const u64 c0 = s[0] ^ s[5] ^ s[10] ^ s[15] ^ s[20];
     const u64 c1 = s[1] ^ s[6] ^ s[11] ^ s[16] ^ s[21];
