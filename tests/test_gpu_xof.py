@@ -67,3 +67,17 @@ def test_xof_argument_errors():
     assert lib.ck_xof_uniform(None, None, 0, None, -1, 4, out.data_ptr(), None) == _lib.CK_ERR_ARG
     assert lib.ck_xof_uniform(None, None, 0, None, 1, 4, out.data_ptr(), None) == _lib.CK_ERR_ARG
     assert lib.ck_expand_key_a(None, None, None, 0, 1, None, None) == _lib.CK_ERR_ARG
+
+
+def test_expand_key_both_kernel_forms_agree():
+    """ck_expand_key_a picks one warp per row up to ~3,000 rows and one thread per
+    row above: the same keys expanded in a large batch (thread form) and alone
+    (warp form) must agree, and the reference-pinned keys sit in both."""
+    p = config("C3").params
+    seeds = list(xof_cases.KEY_SEEDS) + [b"rot%d" % k + (7).to_bytes(8, "little") for k in range(40)]
+    big = ckks.expand_key_a(p, seeds)            # > 40 keys x 96 rows -> thread per row
+    for k in (0, 1, 20, len(seeds) - 1):
+        small = ckks.expand_key_a(p, [seeds[k]])  # 96 rows -> warp per row
+        assert torch.equal(big[k], small[0]), k
+    for k in range(len(xof_cases.KEY_SEEDS)):
+        assert digest(to_host(big[k])) == GOLD[f"key_C3_{k}"], k
