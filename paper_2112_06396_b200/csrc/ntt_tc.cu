@@ -276,11 +276,14 @@ constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof
 
 template <int P2, bool INV>
 int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  // the shared-memory opt-in is per device: track it per device ordinal
+  static unsigned done = 0;  // bit d: set on device d (ordinals < 32)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !((done >> dev) & 1u)) {
     cudaFuncSetAttribute(ntt_col_tc_kernel<P2, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kTcSmem);
-    attr = true;
+    if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);
   }
   const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
   launch_pdl(ntt_col_tc_kernel<P2, INV>, grid, dim3(kTcThreads), kTcSmem, st, a);
