@@ -1,17 +1,21 @@
-// Forward NTT column phase on the 5th-generation tensor cores (tcgen05.mma
-// kind::i8, accumulators in TMEM).
+// NTT column phase (forward and inverse) on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM).
 //
-// The column phase (stages m = 1 .. 128 of the reference's Cooley-Tukey
-// ladder, rnspoly.py:48-62, on the 256 x 2^P2 storage matrix) maps every
-// column c through the SAME 256 x 256 matrix.  Split by row bits
+// Forward: the column phase (stages m = 1 .. 128 of the reference's
+// Cooley-Tukey ladder, rnspoly.py:48-62, on the 256 x 2^P2 storage matrix)
+// maps every column c through the SAME 256 x 256 matrix.  Split by row bits
 // r = 16 r_hi + r_lo:
 //   stages m = 1..8   mix r_hi only, with twiddles that depend on r_hi alone:
 //                     one 16 x 16 matrix M1, shared by every (r_lo, c);
 //   stages m = 16..128 mix r_lo inside block beta = r_hi; that block evaluates
 //                     mod (X^16 - gamma_beta), i.e. M2[beta] = F diag(d_beta)
-//                     with F = M2[0] and a per-(beta, r_lo) twist d_beta
-//                     (the plan derives F and d from the twiddle table and
-//                     verifies the factorisation entry by entry).
+//                     with F = M2[0] and a per-(beta, r_lo) twist d_beta.
+// Inverse (Gentleman-Sande, rnspoly.py:64-79): blocks first, M1[beta] =
+// diag(e_beta) G on r_lo (an output twist), then one shared matrix on r_hi;
+// the INTT's n^-1 (times ihat) is a Shoup multiply in the last epilogue.
+// The plan derives every matrix and twist from its twiddle tables and checks
+// the factorisations entry by entry (ntt_tc_tables).
+//
 // Each 16-point product is an exact integer GEMM on bytes: with x = sum_a
 // x_a 2^8a and B[(j,a)][(k,b)] = byte b of (Mat[k][j] 2^8a mod p),
 //   S_kb = sum_(j,a) x_ja B[(j,a)][(k,b)]     (K = 128 bytes, < 2^23)
@@ -20,14 +24,18 @@
 // allowed, and the epilogue reduces V = sum_b S_kb 2^8b < 2^80 once (FP64
 // quotient, as in the tensor-core base conversion).
 //
-// CTA = 16 columns x 256 rows of one limb (32 KB), 256 threads:
-//   load tile -> A1[(r_lo,c)][r_hi]        (256 x 128 B, canonical K-major)
-//   MMA  D1 = A1 . B1^T                     (2 x M128 N128 K128, TMEM cols 0..255)
-//   epilogue: y = (V mod p) * d_beta[r_lo]  -> A2[(beta,c)][r_lo]
+// Work unit = a tile of 8 columns x 256 rows of one limb; one CTA (1,024
+// threads, one per SM: 164 KB SMEM, all 512 TMEM columns) runs 4 independent
+// 8-warp pipelines over 32 tiles, sharing B1/B2 and the twists:
+//   cp.async tile -> A1[(g1,c)][e1]         (128 x 128 B, canonical K-major)
+//   MMA  D1 = A1 . B1^T                     (M128 N128 K128, 128 TMEM columns)
+//   epilogue: y = (V mod p) * twist         -> A2[(o,c)][g1]   (same buffer)
 //   MMA  D2 = A2 . B2^T
-//   epilogue: V mod p, lazy in (0, 2p)      -> global rows 16 beta + k
-// Output is lazy in (0, 2p) (the butterfly kernels leave [0, 16q)); every
-// consumer folds either.
+//   epilogue: V mod p                       -> global (forward: lazy (0, 2p);
+//                                              inverse: times the scale, canonical)
+// with the next tile's operand already streaming into the group's second
+// buffer.  Forward outputs are lazy (the butterfly kernels leave [0, 16q));
+// every consumer folds either.
 #include "ck_internal.h"
 #include "ntt.cuh"
 
