@@ -167,7 +167,8 @@ def run_reference(args, rank: int):
     if rank != 0:
         return
     from paper_2112_06396_b200.params import config, galois_exponents
-    p = config("C3").params
+    wl = config("C3")
+    p = wl.params
     allk = galois_exponents(p.n_ring, 64, SEED)
     pool, workers = cpu_pool()
     units = list(range(workers))
@@ -187,7 +188,9 @@ def run_reference(args, rank: int):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded counter-based residues)",
-        "config": {"workload": "C3: 64 independent rotation key-switches, N=2^16, L=24x54b, dnum=3, K=8x60b"},
+        # the same workload identification as our arm's line (run_ours)
+        "config": {"workload": wl.desc, "limbs": p.limbs, "special": len(p.special), "dnum": p.dnum,
+                   "log_n": p.logn, "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
