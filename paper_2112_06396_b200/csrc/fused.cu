@@ -75,8 +75,12 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const 
 // NTT exchange buffer and then holds its natural-order row, so the
 // automorphism gather happens at MAC time (one permutation index per element,
 // shared by all digits) -- no separate staging buffer.
-template <int P1, int P2, int BETA>
+// EXTRA: the timing-experiment (a.dbg) and inline special-INTT (a.intt_special)
+// paths are compiled in; the production instantiation leaves them out.
+template <int P1, int P2, int BETA, bool EXTRA>
 __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_row_kernel(KsRowArgs a) {
+  const int dbg = EXTRA ? a.dbg : 0;
+  const bool intt_special = EXTRA && a.intt_special;
   using F = FusedCfg<P2, kKsEpc>;
   constexpr int LOGN = P1 + P2;
   constexpr int SLOT = F::TR * F::RS;
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
     u64* srow = fsm + d * SLOT + rl * F::RS;
     u64 x[kE];
-    if (own || (a.dbg & 1)) {
+    if (own || (dbg & 1)) {
       const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
 #pragma unroll
       for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       yb[d] = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + 2 * (int)threadIdx.x));
     }
 #pragma unroll 1
-    for (int m = 0; m < ((a.dbg & 2) ? 0 : ITER); ++m) {
+    for (int m = 0; m < ((dbg & 2) ? 0 : ITER); ++m) {
       const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
       ulonglong2 na[BETA], nb[BETA];
       if (m + 1 < ITER) {
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     }
   } else {
 #pragma unroll 2
-  for (int m = 0; m < ((a.dbg & 2) ? 0 : ITER); ++m) {
+  for (int m = 0; m < ((dbg & 2) ? 0 : ITER); ++m) {
     const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
     const int er = e >> P2, ec = e & (F::S - 1);
     const int rr = blockIdx.x * F::TR + er;
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
   }
   }
-  if (a.intt_special && i >= a.l && !(a.dbg & 4)) {
+  if (intt_special && i >= a.l && !(dbg & 4)) {
     // first half of ModDown's INTT on the special rows: re-read the row this
     // CTA just wrote (L1/L2 hit; __syncthreads orders the global accesses),
     // inverse row phase, overwrite lazily in [0, 2q)
@@ -525,11 +529,17 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
     }
   }
   const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
-  auto kern = a.beta == 1   ? ks_row_kernel<P1, P2, 1>
-              : a.beta == 2 ? ks_row_kernel<P1, P2, 2>
-              : a.beta == 3 ? ks_row_kernel<P1, P2, 3>
-              : a.beta == 4 ? ks_row_kernel<P1, P2, 4>
-                            : ks_row_kernel<P1, P2, 0>;
+  const bool extra = a.dbg || a.intt_special;
+  auto kern = extra ? (a.beta == 1   ? ks_row_kernel<P1, P2, 1, true>
+                       : a.beta == 2 ? ks_row_kernel<P1, P2, 2, true>
+                       : a.beta == 3 ? ks_row_kernel<P1, P2, 3, true>
+                       : a.beta == 4 ? ks_row_kernel<P1, P2, 4, true>
+                                     : ks_row_kernel<P1, P2, 0, true>)
+                    : (a.beta == 1   ? ks_row_kernel<P1, P2, 1, false>
+                       : a.beta == 2 ? ks_row_kernel<P1, P2, 2, false>
+                       : a.beta == 3 ? ks_row_kernel<P1, P2, 3, false>
+                       : a.beta == 4 ? ks_row_kernel<P1, P2, 4, false>
+                                     : ks_row_kernel<P1, P2, 0, false>);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(kern, dim3((1 << P1) / F::TR, batch, rows), dim3(F::NT), smem, st, a);
