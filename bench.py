@@ -451,16 +451,46 @@ def run_config(args, rank: int, world: int, local_rank: int):
     for _ in range(args.warmup):
         job.run()
     torch.cuda.synchronize()
+    # Launch-bound configs (C1: one N=2^12 key-switch is ~10 short kernels) replay
+    # one step captured as a CUDA graph; every replay runs the full step.
+    graph = None
+    use_graph = args.graph if args.graph is not None else args.config == "C1"
+    if use_graph:
+        n_cap = lib.ck_launch_count()
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                job.run()
+        torch.cuda.current_stream().wait_stream(cap)
+        launches_per_step = lib.ck_launch_count() - n_cap
+        if hasattr(job, "out_a"):  # the replay must redo the work: clear, replay, compare
+            ref = (job.out_a.clone(), job.out_b.clone())
+            job.out_a.zero_()
+            job.out_b.zero_()
+            graph.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(job.out_a, ref[0]) and torch.equal(job.out_b, ref[1]), \
+                "CUDA-graph replay does not reproduce the step"
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     n0 = lib.ck_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        job.run()
+        if graph is not None:
+            graph.replay()
+        else:
+            job.run()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    launches = (launches_per_step * args.steps if graph is not None
+                else lib.ck_launch_count() - n0)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -480,11 +510,12 @@ def run_config(args, rank: int, world: int, local_rank: int):
             "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, generated on device)",
-            "config": {"workload": wl.desc, "units_per_gpu_per_step": per_step},
+            "config": {"workload": wl.desc, "units_per_gpu_per_step": per_step,
+                       "cuda_graph": graph is not None},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "algorithmic_bytes_per_unit": bytes_unit, "peak_kind": peak_kind},
-            "gpu_launches": lib.ck_launch_count() - n0, **extra}), flush=True)
+            "gpu_launches": launches, **extra}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -497,6 +528,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--graph", type=int, default=None,
+                    help="replay a CUDA-graph capture of one step (non-C3 configs; default: C1 only)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=4)
     ap.add_argument("--e2e-chunk-compressed", type=int, default=8)
