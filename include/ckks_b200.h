@@ -120,6 +120,17 @@ int ck_rotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const u
               int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
               ck_stream stream);
 
+/* ---- relinearisation key-switch of new_mult (ckks.py:639-651) ----
+ * (a3, b3, c3) at `level` chain limbs (value_mult / addend / const already
+ * folded into b3, c3 by the caller, ckks.py:624-638) ->
+ *   digits = ModUp(a3); (u, v) = KSKIP(digits, relin key, t = 1);
+ *   u += pmodup(b3); v += pmodup(c3);  out = ModDown by P * q_last (l-1 limbs).
+ * level >= 2; outputs [level-1][N] each.  One call: no host round trips.    */
+size_t ck_relin_workspace_bytes(const ck_plan* plan, int level);
+int ck_relin(const ck_plan* plan, const uint64_t* a3, const uint64_t* b3, const uint64_t* c3,
+             const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a,
+             uint64_t* out_b, uint64_t* workspace, ck_stream stream);
+
 /* ---- hoisted rotations (ckks.hrotate, ckks.py:655-667) ----
  * One shared ModUp of a; n_rot KSKIPs in one launch (shared evaluation-form
  * digits, per-rotation key [n_rot][dnum][L+K][N] and Galois element, DEVICE

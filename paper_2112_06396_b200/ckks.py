@@ -317,13 +317,21 @@ def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext,
         c3 = c3.add(ad.b.mul_scalars(scal))
     if const:
         c3 = c3.add(_const_poly(c3.moduli, params.n_ring, round(const * prod_delta)))
-    digits = _decomp_modup(params, a3)
-    u_hat, v_hat = _kskip(params, digits, keys.relin)
-    u_hat = u_hat.add(pmodup(params, b3))
-    v_hat = v_hat.add(pmodup(params, c3))
-    a_out = _moddown_merged(params, u_hat, lim)
-    b_out = _moddown_merged(params, v_hat, lim)
-    return Ciphertext(a_out, b_out, prod_delta / u_hat.moduli[lim - 1])
+    # ModUp(a3) -> KSKIP(relin) -> + pmodup(b3, c3) -> ModDown by P*q_last (ckks.py:639-651)
+    # as one C-ABI call (ck_relin)
+    assert a3.moduli == params.chain[:lim] and lim >= 2
+    plan = plan_for(params)
+    n = params.n_ring
+    out = torch.empty((2, lim - 1, n), dtype=torch.uint64, device="cuda")
+    nbytes = _L().ck_relin_workspace_bytes(plan.h, lim)
+    assert nbytes > 0
+    ws = torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
+    key = keys.relin
+    check(_L().ck_relin(plan.h, ptr(a3.data), ptr(b3.data), ptr(c3.data), ptr(key.b), ptr(key.a), lim,
+                        ptr(out[0]), ptr(out[1]), ptr(ws), stream_handle()), "ck_relin")
+    mods = params.chain[:lim - 1]
+    return Ciphertext(RnsPoly(mods, out[0], "eval"), RnsPoly(mods, out[1], "eval"),
+                      prod_delta / params.chain[lim - 1])
 
 
 # ------------------------------------------- plaintext-constant operations

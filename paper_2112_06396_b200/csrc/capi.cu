@@ -1086,6 +1086,46 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
                 level, batch, st);
 }
 
+size_t ck_relin_workspace_bytes(const ck_plan* p, int level) {
+  if (!level_ok(p, level) || level < 2) return 0;
+  const LevelTab& t = p->lv[level];
+  const size_t rows = (size_t)t.beta * t.R + 2 * (size_t)t.R + (size_t)level;
+  return rows * p->n * sizeof(u64) + ck_workspace_bytes(p, level, 1);
+}
+
+int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const uint64_t* c3_,
+             const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a_,
+             uint64_t* out_b_, uint64_t* workspace_, ck_stream stream) {
+  const u64 *a3 = (const u64*)a3_, *b3 = (const u64*)b3_, *c3 = (const u64*)c3_;
+  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
+  if (!level_ok(p, level) || level < 2 || !a3 || !b3 || !c3 || !key_b || !key_a || !out_a ||
+      !out_b || !ws || p->K < 1)
+    return CK_ERR_ARG;
+  const LevelTab& t = p->lv[level];
+  if (!t.md[1].valid) return CK_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long N = p->n, R = t.R, l = level;
+  u64* dig = ws;                       // [beta][R][N]
+  u64* uv = dig + (long long)t.beta * R * N;  // u [R][N], v [R][N]
+  u64* tmp = uv + 2 * R * N;           // [l][N]
+  u64* w2 = tmp + l * N;               // ck_workspace_bytes(level, 1)
+  CK_TRY(ck_modup(p, a3_, level, (uint64_t*)dig, (uint64_t*)w2, 1, stream));
+  CK_TRY(ck_kskip(p, (const uint64_t*)dig, key_b, key_a, level, 1, nullptr, (uint64_t*)uv,
+                  (uint64_t*)(uv + R * N), 1, stream));
+  // pmodup (ckks.py:478-489): chain rows += [P]_q * x, special rows += 0
+  for (int half = 0; half < 2; ++half) {
+    u64* dst = uv + half * R * N;
+    CK_TRY(ew_run(p, ck::EW_MULC, tmp, 0, half ? c3 : b3, 0, nullptr, 0, nullptr, 0,
+                  t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, 1, st));
+    CK_TRY(ew_run(p, ck::EW_ADD, dst, 0, dst, 0, tmp, 0, nullptr, 0, t.d_chain_prime, nullptr, 1,
+                  nullptr, (int)l, 1, st));
+  }
+  // ModDown by P * q_last (ckks.py:643-651)
+  CK_TRY(ck_moddown(p, (uint64_t*)uv, level, 1, out_a_, nullptr, 1, (uint64_t*)w2, 1, stream));
+  return ck_moddown(p, (uint64_t*)(uv + R * N), level, 1, out_b_, nullptr, 1, (uint64_t*)w2, 1,
+                    stream);
+}
+
 size_t ck_hrotate_workspace_bytes(const ck_plan* p, int level, int n_rot) {
   if (!level_ok(p, level) || n_rot < 1 || p->K < 1) return 0;
   const LevelTab& t = p->lv[level];

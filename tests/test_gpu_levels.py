@@ -115,3 +115,20 @@ def test_pt_matvec_diagonal_sets(offs):
     got = gpu_backend.GpuBackend().pt_matvec(p, a, b, keys, diags)
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
+
+
+def test_relin_argument_errors():
+    """ck_relin (new_mult's fused relinearisation key-switch) rejects bad levels
+    and null operands with CK_ERR_ARG instead of launching."""
+    from paper_2112_06396_b200 import _lib
+    from paper_2112_06396_b200.device import plan_for
+    p = _params(12, 4, 1, 4)
+    lib = _lib.load()
+    h = plan_for(p).h
+    assert lib.ck_relin_workspace_bytes(h, 1) == 0          # merged ModDown needs l >= 2
+    assert lib.ck_relin_workspace_bytes(h, p.limbs) > 0
+    x = torch.zeros((p.limbs, p.n_ring), dtype=torch.uint64, device="cuda")
+    assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), None, None, p.limbs,
+                        x.data_ptr(), x.data_ptr(), x.data_ptr(), None) == _lib.CK_ERR_ARG
+    assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), 1,
+                        x.data_ptr(), x.data_ptr(), x.data_ptr(), None) == _lib.CK_ERR_ARG
