@@ -31,12 +31,15 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
   const int logn = a.logn;
   const int p2 = ks_row_bits(logn);
   const int rowlen = 1 << p2;
-  const int i = blockIdx.y;
-  const long long bz = blockIdx.z;
+  // grid (batch, tile, row): the batch items that share a digit tile (hoisted
+  // rotations: same digits, different keys / Galois elements) run back to back,
+  // so the tile is still in L2 for all of them
+  const int i = blockIdx.z;
+  const long long bz = blockIdx.x;
   const int prime = a.prime[i];
   const PrimeConst P = a.pc[prime];
   const u64 t = a.galois ? a.galois[bz] : a.galois_t;
-  const long long tile0 = (long long)blockIdx.x * TILE;
+  const long long tile0 = (long long)blockIdx.y * TILE;
   const int krow = a.key_row[i];
   const u64* kb = a.key_b + bz * a.key_batch + ((long long)krow << logn);
   const u64* ka = a.key_a + bz * a.key_batch + ((long long)krow << logn);
@@ -121,7 +124,7 @@ int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st) {
   const int n = 1 << a.logn;
   count_launches(1);
   if (n >= 512) {
-    const dim3 g(n / 512, rows, batch);
+    const dim3 g(batch, n / 512, rows);
     if (a.beta == 3) kskip_kernel<512, 3><<<g, kKsThreads, 0, st>>>(a);
     else if (a.beta == 4) kskip_kernel<512, 4><<<g, kKsThreads, 0, st>>>(a);
     else kskip_kernel<512><<<g, kKsThreads, 0, st>>>(a);
@@ -129,7 +132,7 @@ int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st) {
     // small rings: one tile holds the whole limb (row_bits == logn)
     switch (a.logn) {
 #define CK_KS_SMALL(L) \
-  case L: kskip_kernel<(1 << L)><<<dim3(1, rows, batch), kKsThreads, 0, st>>>(a); break;
+  case L: kskip_kernel<(1 << L)><<<dim3(batch, 1, rows), kKsThreads, 0, st>>>(a); break;
       CK_KS_SMALL(1) CK_KS_SMALL(2) CK_KS_SMALL(3) CK_KS_SMALL(4) CK_KS_SMALL(5)
       CK_KS_SMALL(6) CK_KS_SMALL(7) CK_KS_SMALL(8)
 #undef CK_KS_SMALL
