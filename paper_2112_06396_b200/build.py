@@ -13,19 +13,37 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libckks_b200.so")
-SOURCES = ["ntt.cu", "ntt_tc.cu", "bconv.cu", "bccol.cu", "kskip.cu", "ew.cu", "fused.cu", "bsgs.cu", "xof.cu", "capi.cu"]
+SOURCES = ["ntt.cu", "ntt_tc.cu", "bconv.cu", "kskip.cu", "ew.cu", "fused.cu", "bsgs.cu", "xof.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+def _source_hash(extra=()) -> str:
+    """sha256 over every CUDA source/header, the C-ABI header, the flags and nvcc's path."""
+    import hashlib
+    h = hashlib.sha256()
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cuh", ".h")))
     deps.append(os.path.join(os.path.dirname(HERE), "include", "ckks_b200.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+    for d in deps:
+        h.update(os.path.basename(d).encode())
+        h.update(open(d, "rb").read())
+    h.update(" ".join([NVCC, *FLAGS, *extra]).encode())
+    return h.hexdigest()
+
+
+def _stamp(out: str) -> str:
+    return out + ".srchash"
+
+
+def _stale() -> bool:
+    """Rebuild unless the library exists AND was built from exactly these sources
+    (a content hash, not mtimes: a shipped prebuilt .so newer than edited sources
+    would otherwise be reused)."""
+    if not os.path.exists(LIB) or not os.path.exists(_stamp(LIB)):
+        return True
+    return open(_stamp(LIB)).read().strip() != _source_hash()
 
 
 def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
@@ -59,6 +77,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) 
         raise RuntimeError("link failed")
     for o in objs:
         os.remove(o)
+    with open(_stamp(out), "w") as f:
+        f.write(_source_hash(extra) + "\n")
     return out
 
 

@@ -156,25 +156,15 @@ struct LevelTab {
 struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
-  int ks_dbg = 0;     // CKB200_KSDBG: timing experiments only
-  int ks_ws = 0;      // CKB200_KSWS=1: warp-specialised ks_row variant
-  int ks_intt_inline = 0;  // CKB200_KSINTT=1: special-row INTT row phase inside ks_row
-  int key_prefetch = 2;    // CKB200_KPF=k: L2 prefetch of the first k/8 of each key tile in ks_row (k=8: +4 GB DRAM re-reads; k=2 best, -2%)
-  int chunk = 0;      // key-switches per pipeline pass (CKB200_CHUNK; 0 = auto)
-  int nstreams = 1;   // concurrent chunk streams (CKB200_STREAMS)
+  int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
-  int bc_col = 0;     // CKB200_BCCOL=1: conversion fused with the forward column phase (bccol.cu; measured slower)
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
   ulonglong2* d_tcD = nullptr;
-  int ntt_tc_inv = 1;  // CKB200_NTTTC=2: forward column phase only on the tensor cores
   std::vector<u64> mod, psi;
   PrimeConst* d_pc = nullptr;
   u64* d_mod = nullptr;    // full basis chain || special (key-row moduli)
   ulonglong2* d_tw = nullptr;
   ulonglong2* d_itw = nullptr;
-  Tw4* d_ctw = nullptr;   // column-phase twiddles, FP64-assisted form [prime][2^P1]
-  Tw4* d_citw = nullptr;
-  bool fp_ntt = false;    // CKB200_FPNTT=1: FP64-assisted column twiddles (measured slower)
   std::vector<LevelTab> lv;  // index = level
   std::vector<void*> allocs;
   std::vector<ck_bconv*> bcs;
@@ -430,12 +420,9 @@ int ntt_rows(const ck_plan* p, u64* base, const int* prime, const long long* off
   a.batch_stride = bstride;
   a.src = nullptr;
   a.src_batch_stride = 0;
-  a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
-  a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
   a.tcB = p->d_tcB;
   a.tcD = p->d_tcD;
-  a.tc_inv = p->ntt_tc_inv;
   return ck::launch_ntt(a, jobs, batch, inv, st);
 }
 
@@ -453,12 +440,9 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   a.batch_stride = bstride;
   a.src = src;
   a.src_batch_stride = src_bstride;
-  a.ctw = p->fp_ntt ? p->d_ctw : nullptr;
-  a.citw = p->fp_ntt ? p->d_citw : nullptr;
   a.logn = p->logn;
   a.tcB = p->d_tcB;
   a.tcD = p->d_tcD;
-  a.tc_inv = p->ntt_tc_inv;
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
 
@@ -615,26 +599,18 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
                    a_src, l * N));  // row phase reads the ciphertext directly
   CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, t.d_modup_scale, level, B, l * N, true, 1,
                    st));
-  bool modup_done = false;
   if (t.beta <= ck::kMaxBcGroups) {  // all digits' conversions in one launch
     ck::BconvArgs gs[ck::kMaxBcGroups];
     for (int d = 0; d < t.beta; ++d)
       gs[d] = bconv_args(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
                          false);
-    if (p->bc_col && ck::bc_col_supported(gs, t.beta, p->logn)) {
-      // conversion + forward column phase of all targets in one kernel (bccol.cu)
-      CK_TRY(ck::launch_bc_col(gs, t.beta, B, p->d_tw, st));
-      modup_done = true;
-    } else {
-      CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
-    }
+    CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
   } else {
     for (int d = 0; d < t.beta; ++d)
       CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
                        false, B, st));
   }
-  if (!modup_done)
-    CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs,
+  CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs,
                      B, dig_b, false, 1, st));
   // ---- row phase + automorph + KSKIP (+ INTT row phase of the special rows)
   ck::KsRowArgs ka_;
@@ -663,24 +639,17 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ka_.l = level;
   ka_.R = (int)R;
   ka_.logn = p->logn;
-  ka_.intt_special = p->ks_intt_inline ? 1 : 0;
-  ka_.dbg = p->ks_dbg;
-  ka_.ws = p->ks_ws;
   ka_.key_prefetch = p->key_prefetch;
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
-                   true, p->ks_intt_inline ? 1 : 0, st));
+                   true, 0, st));
   {
     const ck::BconvArgs g1 = bconv_args(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv,
                                         l * N, false);
-    if (p->bc_col && ck::bc_col_supported(&g1, 1, p->logn)) {
-      CK_TRY(ck::launch_bc_col(&g1, 1, 2 * B, p->d_tw, st));
-    } else {
-      CK_TRY(ck::launch_bconv(g1, 2 * B, st));
-      CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false,
-                       1, st));
-    }
+    CK_TRY(ck::launch_bconv(g1, 2 * B, st));
+    CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false,
+                     1, st));
   }
   // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
   ck::MdRowArgs ma;
@@ -746,22 +715,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   {
     const char* e = getenv("CKB200_UNFUSED");
     p->fused = !(e && e[0] == '1');
-    const char* d = getenv("CKB200_KSDBG");
-    p->ks_dbg = d ? atoi(d) : 0;
-    const char* kp = getenv("CKB200_KPF");
-    if (kp) p->key_prefetch = atoi(kp);
-    const char* ki = getenv("CKB200_KSINTT");
-    p->ks_intt_inline = ki ? atoi(ki) : 0;
-    const char* wsv = getenv("CKB200_KSWS");
-    p->ks_ws = wsv ? atoi(wsv) : 0;
-    const char* c = getenv("CKB200_CHUNK");
-    if (c) p->chunk = atoi(c);
-    const char* ns = getenv("CKB200_STREAMS");
-    if (ns) p->nstreams = atoi(ns);
     const char* tc = getenv("CKB200_BCTC");
     if (tc) p->bc_tc = atoi(tc);
-    const char* bcc = getenv("CKB200_BCCOL");
-    if (bcc) p->bc_col = atoi(bcc);
   }
   for (int i = 0; i < n_chain; ++i) p->mod.push_back(chain[i]);
   for (int i = 0; i < n_special; ++i) p->mod.push_back(special[i]);
@@ -810,32 +765,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   p->d_mod = upload(p->allocs, p->mod, &err);
   p->d_tw = upload(p->allocs, tw, &err);
   p->d_itw = upload(p->allocs, itw, &err);
-  if (log_n >= 12) {  // split transforms: column phase of 2^P1 points
-    const int p1 = log_n / 2, ct = 1 << p1;
-    std::vector<Tw4> ctw((size_t)np * ct), citw((size_t)np * ct);
-    auto mk = [](u64 w, u64 q) {
-      Tw4 t;
-      t.w0 = w;
-      t.w1 = mulmod_h(w, (u64)1 << 32, q);
-      t.f0 = (double)((long double)t.w0 / (long double)q);
-      t.f1 = (double)((long double)t.w1 / (long double)q);
-      return t;
-    };
-    for (int i = 0; i < np; ++i)
-      for (int k = 0; k < ct; ++k) {
-        ctw[(size_t)i * ct + k] = mk(tw[(size_t)i * N + k].x, p->mod[i]);
-        citw[(size_t)i * ct + k] = mk(itw[(size_t)i * N + k].x, p->mod[i]);
-      }
-    p->d_ctw = upload(p->allocs, ctw, &err);
-    p->d_citw = upload(p->allocs, citw, &err);
-  }
-  {
-    const char* e = getenv("CKB200_FPNTT");
-    p->fp_ntt = e && e[0] == '1';
-  }
   if (log_n == 16 || log_n == 17) {
     const char* e = getenv("CKB200_NTTTC");
-    p->ntt_tc_inv = !(e && e[0] == '2');
     if (!(e && e[0] == '0')) {
       std::vector<unsigned char> tb;
       std::vector<ulonglong2> td;
@@ -1025,52 +956,9 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
     kgal = nullptr;
   }
   if (ck::fused_supported(p->logn) && p->fused) {
-    // Chunked software pipeline: the batch is cut into chunks issued
-    // round-robin on `nstreams` internal streams (forked from / joined to the
-    // caller's stream), each with its own slice of the workspace, so kernels
-    // of different chunks (compute-bound NTT/BC vs. key-streaming KSKIP) can
-    // run concurrently.  Defaults from CKB200_CHUNK / CKB200_STREAMS.
-    const int NS = std::max(1, std::min(p->nstreams, batch));
-    int C = p->chunk > 0 ? std::min(p->chunk, batch) : batch;
-    if (NS > 1 && p->chunk <= 0) C = (batch + 2 * NS - 1) / (2 * NS);
-    const long long kbatch = (long long)p->key_digits * (p->L + p->K) * N;
     const u64* egal = mode == 1 ? nullptr : galois;
-    if (NS == 1) {
-      for (int c0 = 0; c0 < batch; c0 += C) {
-        const int cc = std::min(C, batch - c0);
-        CK_TRY(rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N,
-                            key_b + c0 * kbatch, key_a + c0 * kbatch, kgt,
-                            kgal ? kgal + c0 : nullptr, egt, egal ? egal + c0 : nullptr,
-                            out_a + c0 * l * N, out_b + c0 * l * N, w, cc, st));
-      }
-      return 0;
-    }
-    std::vector<cudaStream_t> ss(NS);
-    std::vector<cudaEvent_t> ev(NS + 1);
-    for (int i = 0; i < NS; ++i) CK_TRY((int)cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking));
-    for (int i = 0; i <= NS; ++i) CK_TRY((int)cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-    CK_TRY((int)cudaEventRecord(ev[NS], st));
-    // per-stream workspace slices (regions sized for C items each; C*NS <= batch)
-    const size_t slice = ck_workspace_bytes(p, level, C) / sizeof(u64);
-    int rc = 0;
-    for (int i = 0; i < NS && !rc; ++i) rc = (int)cudaStreamWaitEvent(ss[i], ev[NS], 0);
-    for (int ci = 0, c0 = 0; c0 < batch && !rc; ++ci, c0 += C) {
-      const int cc = std::min(C, batch - c0);
-      const int si = ci % NS;
-      const Ws wsi = ws_layout(p, level, C, (u64*)workspace + (mode == 1 ? 0 : si * slice) +
-                                                (mode == 1 ? 2LL * batch * l * N + si * slice : 0));
-      rc = rotate_fused(p, level, a_src + c0 * l * N, b_add + c0 * l * N, key_b + c0 * kbatch,
-                        key_a + c0 * kbatch, kgt, kgal ? kgal + c0 : nullptr, egt,
-                        egal ? egal + c0 : nullptr, out_a + c0 * l * N, out_b + c0 * l * N, wsi,
-                        cc, ss[si]);
-    }
-    for (int i = 0; i < NS; ++i) {
-      cudaEventRecord(ev[i], ss[i]);
-      cudaStreamWaitEvent(st, ev[i], 0);
-    }
-    for (int i = 0; i < NS; ++i) cudaStreamDestroy(ss[i]);
-    for (int i = 0; i <= NS; ++i) cudaEventDestroy(ev[i]);
-    return rc;
+    return rotate_fused(p, level, a_src, b_add, key_b, key_a, kgt, kgal, egt, egal, out_a, out_b,
+                        w, batch, st);
   }
   CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
   // uv: [B][2][R][N]

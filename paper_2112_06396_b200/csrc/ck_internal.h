@@ -12,10 +12,6 @@ typedef unsigned long long u64;
 struct PrimeConst {
   u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, nq;
 };
-struct Tw4 {
-  u64 w0, w1;
-  double f0, f1;
-};
 #endif
 
 namespace ck {
@@ -88,10 +84,8 @@ struct KsRowArgs {
   const u64* galois;            // per batch item (nullable: galois_t)
   u64 galois_t;
   int lo[16], hi[16];           // digit spans (chain rows)
-  int beta, l, R, logn, intt_special;
-  int dbg;                      // timing experiments only (CKB200_KSDBG); 0 in production
-  int ws;                       // warp-specialised persistent variant (CKB200_KSWS)
-  int key_prefetch;             // bulk L2 prefetch of the key tile at kernel start (CKB200_KPF)
+  int beta, l, R, logn;
+  int key_prefetch;             // bulk L2 prefetch of the first k/8 of each key tile at kernel start
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
 
@@ -164,11 +158,6 @@ struct BconvGroups {
   BconvArgs g[kMaxBcGroups];
 };
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st);
-// conversion fused with the forward NTT column phase of every target (bccol.cu);
-// tw = the plan's forward twiddle table
-bool bc_col_supported(const BconvArgs* gs, int ng, int logn);
-int launch_bc_col(const BconvArgs* gs, int ng, int batch, const ulonglong2* tw, cudaStream_t st);
-
 // Key-switching inner product with a fused eval-domain automorphism.
 struct KskipArgs {
   const u64* digits;            // [beta][R][N] raised-basis eval rows

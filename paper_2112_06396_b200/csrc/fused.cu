@@ -19,6 +19,7 @@
 #include "ntt.cuh"
 
 #include <algorithm>
+#include <atomic>
 
 namespace ck {
 
@@ -75,18 +76,14 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const 
 // NTT exchange buffer and then holds its natural-order row, so the
 // automorphism gather happens at MAC time (one permutation index per element,
 // shared by all digits) -- no separate staging buffer.
-// EXTRA: the timing-experiment (a.dbg) and inline special-INTT (a.intt_special)
-// paths are compiled in; the production instantiation leaves them out.
-template <int P1, int P2, int BETA, bool EXTRA>
+template <int P1, int P2, int BETA>
 __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_row_kernel(KsRowArgs a) {
-  const int dbg = EXTRA ? a.dbg : 0;
-  const bool intt_special = EXTRA && a.intt_special;
   using F = FusedCfg<P2, kKsEpc>;
   constexpr int LOGN = P1 + P2;
   constexpr int SLOT = F::TR * F::RS;
   extern __shared__ __align__(16) u64 fsm[];
   pdl_trigger();
-  const int i = blockIdx.z;            // grid (row tile, batch, limb): see ks_row_ws_kernel
+  const int i = blockIdx.z;            // grid (row tile, batch, limb): twiddle reuse across the batch
   const long long b = blockIdx.y;
   const int prime = a.prime[i];
   const PrimeConst& P = a.pc[prime];
@@ -146,7 +143,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
     u64* srow = fsm + d * SLOT + rl * F::RS;
     u64 x[kE];
-    if (own || (dbg & 1)) {
+    if (own) {
       const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
 #pragma unroll
       for (int k = 0; k < kE; ++k) x[k] = src[sub_index<P2, 0, false>(g, k)];
@@ -188,7 +185,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       yb[d] = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + 2 * (int)threadIdx.x));
     }
 #pragma unroll 1
-    for (int m = 0; m < ((dbg & 2) ? 0 : ITER); ++m) {
+    for (int m = 0; m < ITER; ++m) {
       const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
       ulonglong2 na[BETA], nb[BETA];
       if (m + 1 < ITER) {
@@ -236,7 +233,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     }
   } else {
 #pragma unroll 2
-  for (int m = 0; m < ((dbg & 2) ? 0 : ITER); ++m) {
+  for (int m = 0; m < ITER; ++m) {
     const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
     const int er = e >> P2, ec = e & (F::S - 1);
     const int rr = blockIdx.x * F::TR + er;
@@ -270,164 +267,6 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
     *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
     *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
   }
-  }
-  if (intt_special && i >= a.l && !(dbg & 4)) {
-    // first half of ModDown's INTT on the special rows: re-read the row this
-    // CTA just wrote (L1/L2 hit; __syncthreads orders the global accesses),
-    // inverse row phase, overwrite lazily in [0, 2q)
-    const ulonglong2* itw = a.itw + ((long long)prime << LOGN);
-    u64* srow = fsm + rl * F::RS;
-    u64 y[kE];
-#pragma unroll 1
-    for (int w = 0; w < 2; ++w) {
-      u64* io = w ? vo : uo;
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kE; ++k) y[k] = io[sub_index<P2, 0, true>(g, k)];
-      row_transform<P2, true, LOGN>(y, g, r << P2, srow, itw, q, two_q);
-#pragma unroll
-      for (int k = 0; k < kE; ++k) io[sub_index<P2, Sched<P2>::np - 1, true>(g, k)] = y[k];
-    }
-  }
-}
-
-// ------------------------------------------------- KSKIP row, warp-specialised
-// Persistent CTAs of two 128-thread warp groups and two SMEM buffers:
-//   group A (NTT):  digits of tile k -> buffer k%2 (loads, row NTT, staging)
-//   group B (MAC):  inner product of tile k-1 from buffer (k-1)%2 with key
-//                   rows streamed from HBM, + INTT row phase of special rows
-// handed over with named barriers (FULL/EMPTY per buffer), so the compute-
-// bound NTT of one tile overlaps the key-streaming MAC of the previous one.
-enum { kBarFull0 = 1, kBarEmpty0 = 3, kBarA = 5, kBarB = 6 };
-
-template <int P1, int P2, int BETA>
-__global__ void __launch_bounds__(2 * FusedCfg<P2, kKsEpc>::NT, 2)
-ks_row_ws_kernel(KsRowArgs a, int total_tiles) {
-  using F = FusedCfg<P2, kKsEpc>;
-  constexpr int LOGN = P1 + P2;
-  constexpr int SLOT = F::TR * F::RS;
-  constexpr int NT = F::NT;
-  constexpr int TPL = (1 << P1) / F::TR;  // row tiles per limb
-  extern __shared__ __align__(16) u64 fsm[];
-  const bool grpA = threadIdx.x < NT;
-  const int tid = grpA ? threadIdx.x : threadIdx.x - NT;
-  const int rl = tid / F::G, g = tid % F::G;
-  int k = 0;
-  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++k) {
-    const int sbuf = k & 1;
-    u64* buf = fsm + sbuf * (BETA * SLOT);
-    // row tile fastest, then batch item, then limb: consecutive tiles share
-    // the limb's prime, so its row twiddles stay in L1/L2 across the batch
-    const int rt = tile % TPL;
-    const int nb = total_tiles / (TPL * a.R);
-    const long long b = (tile / TPL) % nb;
-    const int i = tile / (TPL * nb);
-    const int prime = a.prime[i];
-    const PrimeConst& P = a.pc[prime];
-    const u64 q = P.q, two_q = P.two_q;
-    const u64 t = a.galois ? a.galois[b] : a.galois_t;
-    if (grpA) {
-      // ---------------- producer: digit rows -> NTT row phase -> natural order
-      if (k >= 2) bar_sync_n(kBarEmpty0 + sbuf, 2 * NT);
-      const int r = rt * F::TR + rl;
-      const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
-      const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
-      if (tid < 2 * BETA) {  // keys of this tile toward L2 for group B
-        const int d = tid >> 1;
-        const u64* kbase = (tid & 1) ? a.key_a : a.key_b;
-        prefetch_l2(kbase + b * a.key_batch + d * a.key_digit_stride + ((long long)prime << LOGN) +
-                        ((long long)rt * F::TR << P2),
-                    F::TR * F::S * 8);
-      }
-#pragma unroll 1
-      for (int d = 0; d < BETA; ++d) {
-        const bool own = i < a.l && i >= a.lo[d] && i < a.hi[d];
-        u64* srow = buf + d * SLOT + rl * F::RS;
-        u64 x[kE];
-        if (own) {
-          const u64* src = a.a_eval + b * a.a_batch + ((long long)i << LOGN) + ((long long)sr << P2);
-#pragma unroll
-          for (int kk = 0; kk < kE; ++kk) x[kk] = src[sub_index<P2, 0, false>(g, kk)];
-          row_to_smem<P2, 0, false>(x, g, srow);
-        } else {
-          const u64* src = a.dig + b * a.dig_batch + ((long long)(d * a.R + i) << LOGN) +
-                           ((long long)sr << P2);
-#pragma unroll
-          for (int kk = 0; kk < kE; ++kk) x[kk] = src[sub_index<P2, 0, false>(g, kk)];
-          row_transform<P2, false, LOGN, SyncGroup<kBarA, NT>>(x, g, sr << P2, srow, tw, q, two_q);
-#pragma unroll
-          for (int kk = 0; kk < kE; ++kk) x[kk] = fwd_final(x[kk], q);
-          bar_sync_n(kBarA, NT);
-          row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
-        }
-      }
-      bar_arrive_n(kBarFull0 + sbuf, 2 * NT);
-    } else {
-      // ---------------- consumer: inner product with streamed key rows
-      bar_sync_n(kBarFull0 + sbuf, 2 * NT);
-      const long long tile0 = (long long)rt * F::TR << P2;
-      const u64* ka = a.key_a + b * a.key_batch + ((long long)prime << LOGN) + tile0;
-      const u64* kb = a.key_b + b * a.key_batch + ((long long)prime << LOGN) + tile0;
-      u64* ubase = a.uv + b * a.uv_batch + ((long long)i << LOGN);
-      constexpr int ITER = (F::TR * F::S) / (2 * NT);
-#pragma unroll 2
-      for (int m = 0; m < ITER; ++m) {
-        const int e = 2 * tid + 2 * NT * m;
-        const int er = e >> P2, ec = e & (F::S - 1);
-        const int rr = rt * F::TR + er;
-        int sc[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          sc[h] = t == 1 ? ec + h
-                         : (int)(automorph_src(((u32)rr << P2) + ec + h, (u32)t, LOGN) & (F::S - 1));
-        Acc3 su[2], sv[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          acc3_zero(su[h]);
-          acc3_zero(sv[h]);
-        }
-#pragma unroll
-        for (int d = 0; d < BETA; ++d) {
-          const ulonglong2 ya = __ldg((const ulonglong2*)(ka + d * a.key_digit_stride + e));
-          const ulonglong2 yb = __ldg((const ulonglong2*)(kb + d * a.key_digit_stride + e));
-          const u64* drow = buf + d * SLOT + er * F::RS;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const u64 x = drow[sidx(sc[h])];
-            const u64 ax = h ? ya.y : ya.x, bx = h ? yb.y : yb.x;
-            const u32 x0 = lo30(x), x1 = hi30(x);
-            acc3_mac(su[h], x0, x1, lo30(ax), hi30(ax));
-            acc3_mac(sv[h], x0, x1, lo30(bx), hi30(bx));
-          }
-        }
-        u64* uw = ubase + tile0 + e;
-        *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
-        *(ulonglong2*)(uw + a.v_off) =
-            make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
-      }
-      if (a.intt_special && i >= a.l) {
-        const int r = rt * F::TR + rl;
-        const ulonglong2* itw = a.itw + ((long long)prime << LOGN);
-        u64* srow = buf + rl * F::RS;  // buffer slot 0 as exchange space
-        u64* uo = ubase + ((long long)r << P2);
-        u64 y[kE];
-#pragma unroll 1
-        for (int w = 0; w < 2; ++w) {
-          u64* io = w ? uo + a.v_off : uo;
-          bar_sync_n(kBarB, NT);
-#pragma unroll
-          for (int kk = 0; kk < kE; ++kk) y[kk] = io[sub_index<P2, 0, true>(g, kk)];
-          row_transform<P2, true, LOGN, SyncGroup<kBarB, NT>>(y, g, r << P2, srow, itw, q, two_q);
-#pragma unroll
-          for (int kk = 0; kk < kE; ++kk) io[sub_index<P2, Sched<P2>::np - 1, true>(g, kk)] = y[kk];
-        }
-      }
-      bar_arrive_n(kBarEmpty0 + sbuf, 2 * NT);
-    }
-  }
-  // drain: the producer consumes the consumer's last EMPTY arrival per buffer
-  if (grpA) {
-    for (int s2 = 0; s2 < 2 && s2 < k; ++s2) bar_sync_n(kBarEmpty0 + ((k - 1 - s2) & 1), 2 * NT);
   }
 }
 
@@ -502,46 +341,28 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
 }
 
 // ------------------------------------------------------------------ launch
-template <int P1, int P2, int BETA>
-static void launch_ks_ws(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
-  using F = FusedCfg<P2, kKsEpc>;
-  const size_t smem = (size_t)2 * BETA * F::TR * F::RS * 8;
-  auto kern = ks_row_ws_kernel<P1, P2, BETA>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * F::NT, smem);
-  const int total = ((1 << P1) / F::TR) * rows * batch;
-  const int grid = std::min(total, sms * std::max(per_sm, 1));
-  kern<<<grid, 2 * F::NT, smem, st>>>(a, total);
-}
-
 template <int P1, int P2>
 static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2, kKsEpc>;
-  if (a.ws && !a.dbg && a.beta >= 1 && a.beta <= 4) {
-    switch (a.beta) {
-      case 1: launch_ks_ws<P1, P2, 1>(a, rows, batch, st); return 0;
-      case 2: launch_ks_ws<P1, P2, 2>(a, rows, batch, st); return 0;
-      case 3: launch_ks_ws<P1, P2, 3>(a, rows, batch, st); return 0;
-      default: launch_ks_ws<P1, P2, 4>(a, rows, batch, st); return 0;
+  const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
+  const int bsel = a.beta <= 4 ? a.beta : 0;
+  auto kern = bsel == 1   ? ks_row_kernel<P1, P2, 1>
+              : bsel == 2 ? ks_row_kernel<P1, P2, 2>
+              : bsel == 3 ? ks_row_kernel<P1, P2, 3>
+              : bsel == 4 ? ks_row_kernel<P1, P2, 4>
+                          : ks_row_kernel<P1, P2, 0>;
+  if (smem > 48 * 1024) {
+    // the opt-in is per (device, kernel): set it once (host cost on the launch-bound C1 path)
+    static std::atomic<unsigned> done[5];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = dev < 32 ? 1u << dev : 0u;
+    if (!bit || !(done[bsel].load(std::memory_order_relaxed) & bit)) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((size_t)(bsel ? bsel : 8) * F::TR * F::RS * 8));
+      done[bsel].fetch_or(bit, std::memory_order_relaxed);
     }
   }
-  const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
-  const bool extra = a.dbg || a.intt_special;
-  auto kern = extra ? (a.beta == 1   ? ks_row_kernel<P1, P2, 1, true>
-                       : a.beta == 2 ? ks_row_kernel<P1, P2, 2, true>
-                       : a.beta == 3 ? ks_row_kernel<P1, P2, 3, true>
-                       : a.beta == 4 ? ks_row_kernel<P1, P2, 4, true>
-                                     : ks_row_kernel<P1, P2, 0, true>)
-                    : (a.beta == 1   ? ks_row_kernel<P1, P2, 1, false>
-                       : a.beta == 2 ? ks_row_kernel<P1, P2, 2, false>
-                       : a.beta == 3 ? ks_row_kernel<P1, P2, 3, false>
-                       : a.beta == 4 ? ks_row_kernel<P1, P2, 4, false>
-                                     : ks_row_kernel<P1, P2, 0, false>);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(kern, dim3((1 << P1) / F::TR, batch, rows), dim3(F::NT), smem, st, a);
   return 0;
 }

@@ -39,24 +39,12 @@ CK_D u64 shoup_lazy(u64 x, u64 w, u64 wp, u64 q) {
 CK_D u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
 
 // NTT twiddle product in [0, 2q) for any 64-bit x (same contract as
-// shoup_lazy).  The Shoup quotient drops x0*wp0 and the low halves of the
-// two cross products: qa = x1 wp1 + hi(x1 wp0) + hi(x0 wp1) is at most 2
-// below floor(x wp / 2^64), so x w - qa q lies in [0, 4q) and one csub(2q)
-// restores [0, 2q).  Integer cost: 2 IMAD.HI + 1 IMAD.WIDE for the quotient
-// instead of a full 64x64 mulhi (4 IMAD.WIDE + carries); the correction runs
-// on the ALU pipe.  Needs q < 2^62.  Measured 39% SLOWER on C3 (the extra
-// live values push the 64-register NTT kernels into local-memory spills), so
-// it is opt-in (-DCKB200_APPROX_SHOUP); the default is the exact Shoup product.
+// shoup_lazy).  A variant with an approximate quotient (dropping the low
+// partial products) was measured 39% slower on C3 (register spills in the
+// 64-register NTT kernels) and removed; see DESIGN.md.
 CK_D u64 madw(u32 a, u32 b, u64 acc);
 CK_D u64 shoup_tw(u64 x, u64 w, u64 wp, u64 q, u64 two_q) {
-#ifdef CKB200_APPROX_SHOUP
-  const u32 x0 = (u32)x, x1 = (u32)(x >> 32), p0 = (u32)wp, p1 = (u32)(wp >> 32);
-  const u64 qa = madw(x1, p1, (u64)__umulhi(x1, p0)) + __umulhi(x0, p1);
-  const u64 r = x * w - qa * q;
-  return r >= two_q ? r - two_q : r;
-#else
   return x * w - __umul64hi(x, wp) * q;
-#endif
 }
 
 CK_D u64 shoup(u64 x, u64 w, u64 wp, u64 q) { return csub(shoup_lazy(x, w, wp, q), q); }
@@ -156,35 +144,3 @@ CK_D void cp_async8(void* smem, const void* gmem) {
 CK_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 CK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// ---- FP64-assisted constant multiplication (NTT twiddles) ----
-// y * w mod q for any 64-bit y, split as y = y0 + y1 2^32:
-//   y w == y0 W0 + y1 W1 (mod q),  W0 = w, W1 = w 2^32 mod q.
-// Each 32-bit-quotient q_k = round(y_k * (W_k/q)) comes from ONE DFMA on the
-// otherwise idle FP64 pipe (magic-number rounding: fma(y_k, f_k, 1.5*2^52)
-// leaves round(y_k f_k) in the low mantissa bits; |q_k - y_k W_k/q| <= 1/2 +
-// 2^-21 since y_k < 2^32 is exact and f_k = fl(W_k/q)).  The residual
-// y0 W0 + y1 W1 - (q0 + q1) q is then exact mod 2^64 and lies in
-// (-(1+2^-20) q, (1+2^-20) q): adding 2q gives (0, 4q).  Integer work: four
-// 32x64 products (12 IMAD slots) instead of a 64x64 mulhi + two mullo (~19).
-struct Tw4 {
-  u64 w0, w1;
-  double f0, f1;
-};
-
-CK_D double u32_to_double(u32 v) {
-  return __hiloint2double(0x43300000, (int)v) - 4503599627370496.0;  // exact
-}
-
-CK_D u64 fshoup4(u64 y, const Tw4& t, u64 q, u64 nq) {
-  const u32 y0 = (u32)y, y1 = (u32)(y >> 32);
-  const double M = 6755399441055744.0;  // 1.5 * 2^52
-  const u32 q0 = (u32)__double2loint(__fma_rn(u32_to_double(y0), t.f0, M));
-  const u32 q1 = (u32)__double2loint(__fma_rn(u32_to_double(y1), t.f1, M));
-  u64 r = 2 * q;
-  r += (u64)y0 * t.w0;
-  r += (u64)q0 * nq;
-  r += (u64)y1 * t.w1;
-  r += (u64)q1 * nq;
-  return r;  // in (0, 4q)
-}

@@ -2,7 +2,6 @@
 #include "ntt.cuh"
 #include "ck_internal.h"
 
-#include <type_traits>
 
 namespace ck {
 
@@ -15,20 +14,17 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 #ifndef CKB200_NTT_MINB
 #define CKB200_NTT_MINB 3
 #endif
-template <int P1, int P2, bool INV, bool FP>
-__global__ void __launch_bounds__(kTC * (1 << P1) / kE, FP ? 3 : CKB200_NTT_MINB)
+template <int P1, int P2, bool INV>
+__global__ void __launch_bounds__(kTC * (1 << P1) / kE, CKB200_NTT_MINB)
 ntt_col_kernel(NttArgs a) {
   constexpr int S = 1 << P1;
   constexpr int NP = Sched<P1>::np;
   __shared__ u64 sm[S * kTC];
-  __shared__ typename std::conditional<FP, Tw4, ulonglong2>::type tws[S];
+  __shared__ ulonglong2 tws[S];
   const int job = blockIdx.y;
   const int prime = a.prime_idx[job];
-  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q, nq = a.pc[prime].nq;
-  if constexpr (FP) {
-    const Tw4* tw = (INV ? a.citw : a.ctw) + ((long long)prime << P1);
-    for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
-  } else {
+  const u64 q = a.pc[prime].q, two_q = a.pc[prime].two_q;
+  {
     const ulonglong2* tw = (INV ? a.itw : a.tw) + ((long long)prime << a.logn);
     for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
   }
@@ -39,9 +35,7 @@ ntt_col_kernel(NttArgs a) {
 #pragma unroll
   for (int r = 0; r < kE; ++r) x[r] = base[((long long)sub_index<P1, 0, INV>(g, r) << P2) + c];
   __syncthreads();
-#define CK_COL_PASS(PP)                                                        \
-  if constexpr (FP) run_pass_fp<P1, PP, INV, P1 + P2, P2>(x, g, c, tws, q, two_q, nq); \
-  else run_pass<P1, PP, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
+#define CK_COL_PASS(PP) run_pass<P1, PP, INV, true, P1 + P2, P2>(x, g, c, tws, q, two_q);
   CK_COL_PASS(0)
   if constexpr (NP > 1) {
 #pragma unroll
@@ -214,22 +208,19 @@ static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int ph
   const dim3 grow((1 << P1) / R::TR, batch, jobs), brow(R::TR * R::G);
   const bool col = phase != 2, row = phase != 1;
   count_launches((int)col + (int)row);
-  const bool fp = a.ctw != nullptr;
   if (!inv) {
     if (col && P1 == 8 && a.tcB && launch_ntt_col_tc(a, jobs, batch, false, st) == 0) {
       // forward column phase ran on the tensor cores (ntt_tc.cu)
     } else if (col) {
-      if (fp) ntt_col_kernel<P1, P2, false, true><<<gcol, bcol, 0, st>>>(a);
-      else ntt_col_kernel<P1, P2, false, false><<<gcol, bcol, 0, st>>>(a);
+      ntt_col_kernel<P1, P2, false><<<gcol, bcol, 0, st>>>(a);
     }
     if (row) launch_pdl(ntt_row_kernel<P1, P2, false>, grow, brow, 0, st, a);
   } else {
     if (row) launch_pdl(ntt_row_kernel<P1, P2, true>, grow, brow, 0, st, a);
-    if (col && P1 == 8 && a.tcB && a.tc_inv && launch_ntt_col_tc(a, jobs, batch, true, st) == 0) {
+    if (col && P1 == 8 && a.tcB && launch_ntt_col_tc(a, jobs, batch, true, st) == 0) {
       // inverse column phase ran on the tensor cores (ntt_tc.cu)
     } else if (col) {
-      if (fp) ntt_col_kernel<P1, P2, true, true><<<gcol, bcol, 0, st>>>(a);
-      else ntt_col_kernel<P1, P2, true, false><<<gcol, bcol, 0, st>>>(a);
+      ntt_col_kernel<P1, P2, true><<<gcol, bcol, 0, st>>>(a);
     }
   }
 }

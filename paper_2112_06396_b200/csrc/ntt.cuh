@@ -37,13 +37,10 @@ struct NttArgs {
   long long batch_stride;      // elements between batch items (grid.z)
   const u64* src;              // row kernels: read input from here (nullable: in place)
   long long src_batch_stride;  //   with this batch stride (rows at job*N)
-  const Tw4* ctw;              // column-phase twiddles in FP64-assisted form,
-  const Tw4* citw;             //   [prime][2^P1] (nullable: integer Shoup path)
   int logn;
   // tensor-core forward column phase (ntt_tc.cu; nullable: butterfly kernels)
   const unsigned char* tcB = nullptr;  // [prime][2][128 x 128 B] B1 | B2 in SMEM layout
   const ulonglong2* tcD = nullptr;     // [prime][2][16][16] twists {d, d_shoup}
-  int tc_inv = 1;                      // inverse column phase on the tensor cores too
 };
 
 // ---- compile-time pass schedule for a 2^P-point sub-transform ----
@@ -113,56 +110,6 @@ CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict_
       }
     }
   }
-}
-
-CK_D void bfly_ct_fp(u64& X, u64& Y, const Tw4& w, u64 q, u64 two_q, u64 nq) {
-  const u64 t = csub(fshoup4(Y, w, q, nq), two_q);
-  const u64 xx = X;
-  X = xx + t;
-  Y = xx - t + two_q;
-}
-CK_D void bfly_gs_fp(u64& X, u64& Y, const Tw4& w, u64 q, u64 two_q, u64 nq) {
-  const u64 xx = X, yy = Y;
-  X = csub(xx + yy, two_q);
-  Y = csub(fshoup4(xx - yy + two_q, w, q, nq), two_q);
-}
-
-// Same pass with FP64-assisted twiddle products (fshoup4, Tw4 twiddles in
-// shared memory).  The product lands in (0, 4q) and is folded to [0, 2q) with
-// one csub, so the lazy ranges are those of run_pass.  Stages/groups are
-// expanded by template recursion: the FP butterfly is large enough that
-// NVVM's unroller would otherwise keep the loop and spill x[] to local memory.
-template <int P, int p, bool INV, int LOGN, int JSHIFT, int H, int ST>
-CK_D void fp_stage(u64 (&x)[kE], int g, int jbase, const Tw4* __restrict__ tw, u64 q, u64 two_q,
-                   u64 nq) {
-  constexpr int C = Sched<P>::C(p);
-  constexpr int LD = Sched<P>::logD(p, INV);
-  constexpr int lhalf = INV ? ST : (C - 1 - ST);
-  constexpr int half = 1 << lhalf;
-  constexpr int logt = LD + lhalf + JSHIFT;
-  constexpr int logm = LOGN - 1 - logt;
-  const int s0 = sub_index<P, p, INV>(g, H << C);
-#pragma unroll
-  for (int b = 0; b < (1 << C) / (2 * half); ++b) {
-    const int k0 = b * 2 * half;
-    const int j = jbase + ((s0 + (k0 << LD)) << JSHIFT);
-    const Tw4 w = tw[(1 << logm) + (j >> (logt + 1))];
-#pragma unroll
-    for (int k = k0; k < k0 + half; ++k) {
-      if (INV) bfly_gs_fp(x[(H << C) + k], x[(H << C) + k + half], w, q, two_q, nq);
-      else bfly_ct_fp(x[(H << C) + k], x[(H << C) + k + half], w, q, two_q, nq);
-    }
-  }
-  if constexpr (ST + 1 < C) fp_stage<P, p, INV, LOGN, JSHIFT, H, ST + 1>(x, g, jbase, tw, q, two_q, nq);
-}
-
-template <int P, int p, bool INV, int LOGN, int JSHIFT, int H = 0>
-CK_D void run_pass_fp(u64 (&x)[kE], int g, int jbase, const Tw4* __restrict__ tw, u64 q,
-                      u64 two_q, u64 nq) {
-  constexpr int C = Sched<P>::C(p);
-  constexpr int NG = kE >> C;
-  fp_stage<P, p, INV, LOGN, JSHIFT, H, 0>(x, g, jbase, tw, q, two_q, nq);
-  if constexpr (H + 1 < NG) run_pass_fp<P, p, INV, LOGN, JSHIFT, H + 1>(x, g, jbase, tw, q, two_q, nq);
 }
 
 // Forward lazy range maintenance: [0, 16q) -> [0, 8q).

@@ -17,7 +17,8 @@ CPU tests):
   ModDown epilogue on own chain rows) is rank-local.
 
 The limb-sharded algorithm is written once against a small `ops` interface
-(numpy oracle ops in the CPU tests, the CUDA library on the GPU).
+(`TorchOps`: the CUDA library on the GPU; the CPU tests bind the same interface
+to the numpy checker in tests/numpy_ops.py).
 """
 
 from __future__ import annotations
@@ -150,71 +151,6 @@ def keyswitch_limb_sharded(params, shard: LimbShard, a_rows, b_rows, key_b_rows,
         outs.append(y)
     out_b = ops.add(outs[1], ops.automorph(b_rows, galois_t), keep)
     return outs[0], out_b
-
-
-class NumpyOps:
-    """Oracle-backed row ops (CPU tests only)."""
-
-    def __init__(self):
-        from oracle import ckks_np
-        self.o = ckks_np
-
-    def intt(self, x, mods):
-        return self.o.intt(x, mods)
-
-    def ntt(self, x, mods):
-        return self.o.ntt(x, mods)
-
-    def bc_convert(self, x, src, dst):
-        if len(dst) == 0:
-            return np.zeros((0, x.shape[1]), dtype=np.uint64)
-        return self.o.bc_convert(x, src, dst)
-
-    def bc_convert_centered(self, x, src, dst):
-        if len(dst) == 0:
-            return np.zeros((0, x.shape[1]), dtype=np.uint64)
-        return self.o.bc_convert_centered(x, src, dst)
-
-    def automorph(self, x, t):
-        return self.o.automorph(x, t)
-
-    def _q(self, mods):
-        return np.array(mods, dtype=np.uint64)[:, None]
-
-    def mul(self, x, y, mods):
-        return self.o.mulmod(x, y, self._q(mods))
-
-    def add(self, x, y, mods):
-        return self.o.addmod(x, y, self._q(mods))
-
-    def sub(self, x, y, mods):
-        return self.o.submod(x, y, self._q(mods))
-
-    def mul_scalars(self, x, s, mods):
-        return self.o.mulmod(x, np.array(s, dtype=np.uint64)[:, None], self._q(mods))
-
-    def take_rows(self, x, idx):
-        return x[list(idx)]
-
-    def cat_rows(self, parts):
-        return np.concatenate(parts, axis=0)
-
-    # collective helpers (torch tensors on the wire)
-    def pad_rows(self, x, width):
-        import torch
-        out = np.zeros((width, x.shape[1]), dtype=np.uint64)
-        out[:x.shape[0]] = x
-        return torch.from_numpy(out.view(np.int64))
-
-    def empty_like(self, t):
-        import torch
-        return torch.empty_like(t)
-
-    def empty_rows(self, rows, like):
-        return np.zeros((rows, like.shape[1]), dtype=np.uint64)
-
-    def set_row(self, out, row, part, k):
-        out[row] = part[k].numpy().view(np.uint64)
 
 
 class TorchOps:

@@ -31,6 +31,7 @@ def _free_port():
 
 def _setup(rank, world, port):
     sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
@@ -65,6 +66,7 @@ def _batch_worker(rank, world, port, per_rank, out_q):
 def _limb_worker(rank, world, port, pspec, k, out_q):
     _setup(rank, world, port)
     import cases
+    from numpy_ops import NumpyOps
     from paper_2112_06396_b200 import shard, synth
     p = cases.make_params(pspec)
     a, b, kb, ka = synth.rotation_inputs(p, cases.SEED, 3)
@@ -76,7 +78,7 @@ def _limb_worker(rank, world, port, pspec, k, out_q):
     ndig = len(p.digit_spans(L))
     t = pow(5, k, 2 * p.n_ring)
     oa, ob = shard.keyswitch_limb_sharded(
-        p, sh, a[chain], b[chain], kb[:ndig][:, krows], ka[:ndig][:, krows], t, shard.NumpyOps())
+        p, sh, a[chain], b[chain], kb[:ndig][:, krows], ka[:ndig][:, krows], t, NumpyOps())
     got = [None] * world
     dist.all_gather_object(got, (chain, oa, ob))
     if rank == 0:
