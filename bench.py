@@ -441,6 +441,10 @@ def run_config(args, rank: int, world: int, local_rank: int):
         allk = galois_exponents(p.n_ring, B * world, SEED)
         job = W.RotationBatch(p, SEED, units, ks=[allk[u] for u in units])
         per_step, unit, bytes_unit = B, "key-switches/s", ks_bytes(p)
+    elif wl.kind == "relin":
+        B = args.batch
+        job = W.RelinBatch(p, SEED, [rank * B + i for i in range(B)])
+        per_step, unit, bytes_unit = B, "relinearisations/s", job.algorithmic_bytes_per_unit()
     elif wl.kind == "ntt":
         job = W.NttBatch(p, SEED, 16)
         per_step, unit = 16 * p.limbs, "limb NTT+INTT round trips/s"
@@ -520,6 +524,65 @@ def run_config(args, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: start N ranks of this script, one per
+    GPU (RANK / LOCAL_RANK = 0..N-1, rendezvous on 127.0.0.1), exactly as
+    `torch.distributed.run --nproc-per-node N` would; rank 0 prints the line."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(abs(pr.wait()) for pr in procs)
+
+
+def run_selftest(args, rank: int, world: int):
+    """CPU stand-in for the multi-rank harness (gloo): the same rank layout,
+    barrier-bracketed timed region, max-over-ranks reduction and JSON line as
+    run_ours, with each rank's 'step' a fixed host delay instead of the GPU
+    key-switch.  Lets a CPU test check the launcher and the aggregation."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    B = args.batch
+    units = [rank * B + i for i in range(B)]
+    for _ in range(args.warmup):
+        time.sleep(0.001)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.002 * (1 + rank))  # ranks differ: the max must win
+    ms = 1000 * (time.perf_counter() - t0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        seen = torch.tensor([len(units)], dtype=torch.int64)
+        dist.all_reduce(seen)
+        total_units = int(seen.item())
+    else:
+        total_units = len(units)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": total_units * args.steps / (ms / 1000.0),
+                          "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms / args.steps, "selftest": True,
+                          "config": {"units_per_gpu_per_step": B, "global_units_per_step": total_units,
+                                     "parallelism": f"batch-partitioned x{world}"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -527,7 +590,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C3M", "C4", "C5"])
     ap.add_argument("--graph", type=int, default=None,
                     help="replay a CUDA-graph capture of one step (non-C3 configs; default: C1 only)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -540,13 +603,22 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch (default: profiles/r01_traffic.json x units)")
+    ap.add_argument("--selftest-cpu", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to "
+                         "report a world size that was not launched")
     args.batch_set = args.batch is not None
     if args.batch is None:
         args.batch = 64
+    if args.selftest_cpu:
+        run_selftest(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank)
         return

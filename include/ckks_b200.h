@@ -66,8 +66,10 @@ int ck_ntt(const ck_plan* plan, uint64_t* data, const int32_t* prime_idx, int ro
            int64_t batch_stride, int inverse, ck_stream stream);
 
 /* ---- elementwise (RnsPoly.add/sub/mul/neg/mul_scalars, rnspoly.py:182-210) ----
- * op: 0 add, 1 sub, 2 mul, 3 neg, 4 mul by per-row constant, 5 copy.
- * cst: DEVICE {c, floor(c*2^64/q)} pairs per row (op 4 only).             */
+ * op: 0 add, 1 sub, 2 mul, 3 neg, 4 mul by per-row constant, 5 copy,
+ *     6 add per-row constant (encode_const + pt_add, ckks.py:557-568: the
+ *       evaluation form of a degree-0 polynomial is that residue in every slot).
+ * cst: DEVICE {c, floor(c*2^64/q)} pairs per row (ops 4 and 6).            */
 int ck_poly_op(const ck_plan* plan, int op, uint64_t* out, const uint64_t* x, const uint64_t* y,
                const int32_t* prime_idx, const uint64_t* cst, int rows, ck_stream stream);
 
@@ -125,47 +127,58 @@ int ck_rotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const u
  * folded into b3, c3 by the caller, ckks.py:624-638) ->
  *   digits = ModUp(a3); (u, v) = KSKIP(digits, relin key, t = 1);
  *   u += pmodup(b3); v += pmodup(c3);  out = ModDown by P * q_last (l-1 limbs).
- * level >= 2; outputs [level-1][N] each.  One call: no host round trips.    */
-size_t ck_relin_workspace_bytes(const ck_plan* plan, int level);
+ * batch independent products: a3, b3, c3 [batch][level][N], outputs
+ * [batch][level-1][N] each; ONE relinearisation key [dnum][L+K][N] shared by
+ * the batch (KeySet.relin, ckks.py:230).  level >= 2.  Runs the fused
+ * key-switch pipeline of ck_rotate (no automorphism; the pmodup terms fold
+ * into the ModDown epilogue).  No host round trips.                          */
+size_t ck_relin_workspace_bytes(const ck_plan* plan, int level, int batch);
 int ck_relin(const ck_plan* plan, const uint64_t* a3, const uint64_t* b3, const uint64_t* c3,
              const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a,
-             uint64_t* out_b, uint64_t* workspace, ck_stream stream);
-
+             uint64_t* out_b, uint64_t* workspace, int batch, ck_stream stream);
 /* ---- hoisted rotations (ckks.hrotate, ckks.py:655-667) ----
  * One shared ModUp of a; n_rot KSKIPs in one launch (shared evaluation-form
- * digits, per-rotation key [n_rot][dnum][L+K][N] and Galois element, DEVICE
- * uint64[n_rot]); ModDown pairs batched.  Outputs [n_rot][level][N] x 2.      */
+ * digits, per-rotation key and Galois element); ModDown pairs batched.
+ * key_b, key_a: DEVICE arrays of n_rot pointers, each to one switching key's
+ * [dnum][L+K][N] rows (SwitchingKey.b / .a, ckks.py:188-199) -- the keys stay
+ * where the caller keeps them (KeySet.rot, ckks.py:231), nothing is stacked.
+ * galois: DEVICE uint64[n_rot].  Outputs [n_rot][level][N] x 2.              */
 size_t ck_hrotate_workspace_bytes(const ck_plan* plan, int level, int n_rot);
-int ck_hrotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
-               const uint64_t* key_a, const uint64_t* galois, int level, int n_rot,
-               uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, ck_stream stream);
-
+int ck_hrotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b,
+               const uint64_t* const* key_b, const uint64_t* const* key_a,
+               const uint64_t* galois, int level, int n_rot, uint64_t* out_a, uint64_t* out_b,
+               uint64_t* workspace, ck_stream stream);
 /* ---- double-hoisted plaintext matrix-vector product (ckks.pt_matvec, ckks.py:684-719) ----
- * diags: [n_rot + has_identity][level+K][N] raised-basis rows, rotated offsets
- * first (matching key_b/key_a [n_rot][dnum][L+K][N]), identity last; galois:
- * DEVICE uint64[n_rot + has_identity] (identity's element = 1).  One shared
- * ModUp, batched KSKIP, diagonal MAC, one merged ModDown.  Output [level-1][N].  */
+ * Any number of diagonals (the reference takes any dict; a radix-r bootstrap
+ * stage has 2r-1, bootstrap.py:128-133).  diags: DEVICE array of
+ * n_rot + has_identity pointers to [level+K][N] raised-basis rows, rotated
+ * offsets first (matching key_b/key_a, DEVICE pointer arrays [n_rot] as in
+ * ck_hrotate), identity last; galois: DEVICE uint64[n_rot + has_identity]
+ * (identity's element = 1).  One shared ModUp, KSKIP + diagonal MAC in chunks
+ * of <= 32 diagonals accumulating on the raised basis, one merged ModDown.
+ * Output [level-1][N].                                                       */
 size_t ck_pt_matvec_workspace_bytes(const ck_plan* plan, int level, int n_diag);
-int ck_pt_matvec(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
-                 const uint64_t* key_a, const uint64_t* galois, const uint64_t* diags, int level,
-                 int n_rot, int has_identity, uint64_t* out_a, uint64_t* out_b,
-                 uint64_t* workspace, ck_stream stream);
-
+int ck_pt_matvec(const ck_plan* plan, const uint64_t* a, const uint64_t* b,
+                 const uint64_t* const* key_b, const uint64_t* const* key_a,
+                 const uint64_t* galois, const uint64_t* const* diags, int level, int n_rot,
+                 int has_identity, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace,
+                 ck_stream stream);
 /* ---- hoisted BSGS linear transform (composites.py:249-293) ----
  * == sum_{j=1..giant} rotate(pt_matvec(ct, {k: diag[j][k]}), -baby*j)  (ckks.py:684-719)
- * One shared ModUp; `baby` KSKIPs (Galois 5^k, k = 1..baby) in one launch;
+ * One shared ModUp; `baby` KSKIPs (Galois 5^k, k = 1..baby; chunks of <= 32);
  * diagonal MACs into `giant` raised accumulators; merged ModDown (P*q_last);
  * `giant` batched rotations at level-1 (Galois 5^(baby*j)); sum.
- * a, b: [level][N]; baby keys [baby][dnum][L+K][N]; giant keys [giant][...];
- * diags: [giant][baby][level+K][N] raised-basis eval rows; galois arrays DEVICE.
+ * a, b: [level][N]; baby / giant keys: DEVICE pointer arrays [baby] / [giant]
+ * (one [dnum][L+K][N] block each); diags: DEVICE pointer array [giant][baby]
+ * of [level+K][N] raised-basis eval rows; galois arrays DEVICE uint64.
  * Output: [level-1][N] x 2.                                                  */
 size_t ck_bsgs_workspace_bytes(const ck_plan* plan, int level, int baby, int giant);
-int ck_bsgs(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* baby_key_b,
-            const uint64_t* baby_key_a, const uint64_t* giant_key_b, const uint64_t* giant_key_a,
-            const uint64_t* diags, const uint64_t* baby_galois, const uint64_t* giant_galois,
-            int level, int baby, int giant, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace,
-            ck_stream stream);
-
+int ck_bsgs(const ck_plan* plan, const uint64_t* a, const uint64_t* b,
+            const uint64_t* const* baby_key_b, const uint64_t* const* baby_key_a,
+            const uint64_t* const* giant_key_b, const uint64_t* const* giant_key_a,
+            const uint64_t* const* diags, const uint64_t* baby_galois,
+            const uint64_t* giant_galois, int level, int baby, int giant, uint64_t* out_a,
+            uint64_t* out_b, uint64_t* workspace, ck_stream stream);
 /* ---- compressed evaluation keys: SHAKE256 uniform rows (ckks.py:169-215) ----
  * ck_xof_uniform: row r = first n words of SHAKE256(msgs[r][0:msg_lens[r]])
  * (little-endian u64) below floor(2^64/q_r)*q_r, each reduced mod q_r

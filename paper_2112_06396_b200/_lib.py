@@ -39,8 +39,8 @@ _SIGS = [
     ("ck_moddown", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_uint64, vp, C.c_int, vp]),
     ("ck_rotate", C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_uint64, vp, C.c_int, vp, vp, vp,
                             C.c_int, vp]),
-    ("ck_relin_workspace_bytes", C.c_size_t, [vp, C.c_int]),
-    ("ck_relin", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
+    ("ck_relin_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
+    ("ck_relin", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, vp]),
     ("ck_hrotate_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
     ("ck_hrotate", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, vp]),
     ("ck_xof_uniform", C.c_int, [vp, vp, C.c_int64, vp, C.c_int, C.c_int, vp, vp]),

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from ._lib import check
-from .device import plan_for, ptr, shoup_pairs, stream_handle, to_dev
+from .device import const_tensor, plan_for, ptr, ptr_array, shoup_pairs, stream_handle, to_dev
 from .params import CkksParams  # noqa: F401  (re-export, mirrors ckks.CkksParams)
 from .rnspoly import RnsPoly, automorph_rows, ntt_rows
 
@@ -290,9 +290,9 @@ def mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext) -> 
 
 
 def _const_poly(moduli, n: int, integer: int) -> RnsPoly:
-    """encode_const (ckks.py:530-537): NTT of a degree-0 poly = constant in every slot."""
-    vals = np.array([integer % q for q in moduli], dtype=np.uint64)
-    return RnsPoly(moduli, np.repeat(vals[:, None], n, axis=1), "eval")
+    """encode_const (ckks.py:530-537): NTT of a degree-0 poly = constant in every slot
+    (filled on the device: one residue per row crosses PCIe, not an L x N array)."""
+    return RnsPoly.zeros(tuple(moduli), n, "eval").add_scalars([integer % q for q in moduli])
 
 
 def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext, *,
@@ -316,19 +316,20 @@ def new_mult(params: CkksParams, keys: KeySet, ct1: Ciphertext, ct2: Ciphertext,
         b3 = b3.add(ad.a.mul_scalars(scal))
         c3 = c3.add(ad.b.mul_scalars(scal))
     if const:
-        c3 = c3.add(_const_poly(c3.moduli, params.n_ring, round(const * prod_delta)))
+        v = round(const * prod_delta)
+        c3 = c3.add_scalars([v % q for q in c3.moduli])
     # ModUp(a3) -> KSKIP(relin) -> + pmodup(b3, c3) -> ModDown by P*q_last (ckks.py:639-651)
     # as one C-ABI call (ck_relin)
     assert a3.moduli == params.chain[:lim] and lim >= 2
     plan = plan_for(params)
     n = params.n_ring
     out = torch.empty((2, lim - 1, n), dtype=torch.uint64, device="cuda")
-    nbytes = _L().ck_relin_workspace_bytes(plan.h, lim)
+    nbytes = _L().ck_relin_workspace_bytes(plan.h, lim, 1)
     assert nbytes > 0
     ws = torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
     key = keys.relin
     check(_L().ck_relin(plan.h, ptr(a3.data), ptr(b3.data), ptr(c3.data), ptr(key.b), ptr(key.a), lim,
-                        ptr(out[0]), ptr(out[1]), ptr(ws), stream_handle()), "ck_relin")
+                        ptr(out[0]), ptr(out[1]), ptr(ws), 1, stream_handle()), "ck_relin")
     mods = params.chain[:lim - 1]
     return Ciphertext(RnsPoly(mods, out[0], "eval"), RnsPoly(mods, out[1], "eval"),
                       prod_delta / params.chain[lim - 1])
@@ -361,7 +362,8 @@ def encode_const(params: CkksParams, c: float, delta: float, moduli) -> RnsPoly:
 
 def const_add(params: CkksParams, ct: Ciphertext, c: float) -> Ciphertext:
     """ckks.const_add (ckks.py:567-568)."""
-    return pt_add(ct, encode_const(params, c, ct.delta, ct.a.moduli))
+    v = round(c * ct.delta)
+    return Ciphertext(ct.a.copy(), ct.b.add_scalars([v % q for q in ct.b.moduli]), ct.delta)
 
 
 def const_mult_int(ct: Ciphertext, c: int) -> Ciphertext:
@@ -414,7 +416,8 @@ def pt_combo(params: CkksParams, terms, const: float = 0.0) -> Ciphertext:
         acc_a = acc_a.add(ta)
         acc_b = acc_b.add(tb)
     if const:
-        acc_b = acc_b.add(encode_const(params, const, s_pre, mods))
+        v = round(const * s_pre)
+        acc_b = acc_b.add_scalars([v % q for q in mods])
     return Ciphertext(_rescale_poly_p(params, acc_a), _rescale_poly_p(params, acc_b),
                       s_pre / mods[-1])
 
@@ -430,10 +433,10 @@ def hrotate(params: CkksParams, keys: KeySet, ct: Ciphertext, rotations) -> list
     keylist = [keys.rot[r] for r in rotations]  # KeyError like the reference (ckks.py:664)
     plan = plan_for(params)
     n = params.n_ring
-    kb = torch.stack([k.b for k in keylist]).contiguous()
-    ka = torch.stack([k.a for k in keylist]).contiguous()
-    gal = torch.tensor(np.array([_galois(params, r) for r in rotations], dtype=np.uint64),
-                       device="cuda")
+    # per-rotation key pointers: the keys stay where the KeySet holds them
+    kb = ptr_array([k.b for k in keylist])
+    ka = ptr_array([k.a for k in keylist])
+    gal = const_tensor([_galois(params, r) for r in rotations])
     nr = len(rotations)
     out_a = torch.empty((nr, limbs, n), dtype=torch.uint64, device="cuda")
     out_b = torch.empty_like(out_a)
@@ -489,13 +492,15 @@ def pt_matvec(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict,
     keylist = [keys.rot[-off] for off, _ in rot]
     dev = dict(dtype=torch.uint64, device="cuda")
     if keylist:
-        kb = torch.stack([k.b for k in keylist]).contiguous()
-        ka = torch.stack([k.a for k in keylist]).contiguous()
+        kb = ptr_array([k.b for k in keylist])
+        ka = ptr_array([k.a for k in keylist])
     else:
         kb = ka = None
     gal = [_galois(params, -off) for off, _ in rot] + ([1] * len(ident))
-    galt = torch.tensor(np.array(gal, dtype=np.uint64), device="cuda")
-    dg = torch.stack([m.data for _, m in rot] + [m.data for m in ident]).contiguous()
+    galt = const_tensor(gal)
+    for _, m in rot:
+        assert m.data.is_contiguous()
+    dg = ptr_array([m.data for _, m in rot] + [m.data.contiguous() for m in ident])
     out_a = torch.empty((limbs - 1, n), **dev)
     out_b = torch.empty((limbs - 1, n), **dev)
     plan = plan_for(params)
@@ -525,14 +530,13 @@ def bsgs(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict, diag_del
     raised = params.raised_moduli(limbs)
     bkeys = [keys.rot[-k] for k in range(1, baby + 1)]
     gkeys = [keys.rot[-baby * j] for j in range(1, giant + 1)]
-    bkb = torch.stack([k.b for k in bkeys]).contiguous()
-    bka = torch.stack([k.a for k in bkeys]).contiguous()
-    gkb = torch.stack([k.b for k in gkeys]).contiguous()
-    gka = torch.stack([k.a for k in gkeys]).contiguous()
     for jk, d in diags.items():
         assert d.moduli == raised, jk
-    dg = torch.stack([torch.stack([diags[(j, k)].data for k in range(1, baby + 1)])
-                      for j in range(1, giant + 1)]).contiguous()
+        assert d.data.is_contiguous()
+    # pointer arrays: neither keys nor diagonals are copied
+    bkb, bka = ptr_array([k.b for k in bkeys]), ptr_array([k.a for k in bkeys])
+    gkb, gka = ptr_array([k.b for k in gkeys]), ptr_array([k.a for k in gkeys])
+    dg = ptr_array([diags[(j, k)].data for j in range(1, giant + 1) for k in range(1, baby + 1)])
     out_a, out_b = bsgs_raw(params, ct.a.data, ct.b.data, bkb, bka, gkb, gka, dg, baby, giant)
     mods = params.chain[:limbs - 1]
     return Ciphertext(RnsPoly(mods, out_a, "eval"), RnsPoly(mods, out_b, "eval"),
@@ -540,14 +544,13 @@ def bsgs(params: CkksParams, keys: KeySet, ct: Ciphertext, diags: dict, diag_del
 
 
 def bsgs_raw(params, a, b, bkb, bka, gkb, gka, diags, baby: int, giant: int, out=None, ws=None):
-    """ck_bsgs on pre-stacked device tensors (the benchmark's C4 unit)."""
+    """ck_bsgs on device pointer arrays (ptr_array) of the baby / giant keys and
+    the [giant][baby] diagonals (the benchmark's C4 unit)."""
     plan = plan_for(params)
     n = params.n_ring
     limbs = a.shape[0]
-    bgal = torch.tensor(np.array([pow(5, k, 2 * n) for k in range(1, baby + 1)], dtype=np.uint64),
-                        device="cuda")
-    ggal = torch.tensor(np.array([pow(5, baby * j, 2 * n) for j in range(1, giant + 1)],
-                                 dtype=np.uint64), device="cuda")
+    bgal = const_tensor([pow(5, k, 2 * n) for k in range(1, baby + 1)])
+    ggal = const_tensor([pow(5, baby * j, 2 * n) for j in range(1, giant + 1)])
     if out is None:
         out = (torch.empty((limbs - 1, n), dtype=torch.uint64, device="cuda"),
                torch.empty((limbs - 1, n), dtype=torch.uint64, device="cuda"))
@@ -614,7 +617,7 @@ def rotate_batch(params: CkksParams, a: torch.Tensor, b: torch.Tensor, key_b: to
     """
     plan = plan_for(params)
     B, limbs = a.shape[0], a.shape[1]
-    ws = plan.workspace(limbs, B, "batch") if ws is None else ws
+    ws = plan.workspace(limbs, B) if ws is None else ws
     check(_L().ck_rotate(plan.h, ptr(a), ptr(b), ptr(key_b), ptr(key_a), limbs, 1, ptr(galois), 0,
                          ptr(out_a), ptr(out_b), ptr(ws), B, stream_handle()), "ck_rotate")
 
@@ -651,7 +654,7 @@ class HostRotationPipeline:
                          kb=torch.empty((C, dn, full, n), **dev), ka=torch.empty((C, dn, full, n), **dev),
                          oa=torch.empty((C, L, n), **dev), ob=torch.empty((C, L, n), **dev))
                     for _ in range(max(2, min(nbuf, -(-batch // self.chunk))))]
-        self.ws = self.plan.workspace(L, C, "hostpipe")
+        self.ws = self.plan.workspace(L, C)
         self.s_h2d = torch.cuda.Stream()
         self.s_d2h = torch.cuda.Stream()
         self.s_comp = torch.cuda.Stream()

@@ -8,6 +8,8 @@
 // ModUp).  One thread owns one coefficient of one raised row for BOTH the
 // baby inputs (kept in registers) and every giant output, so each diagonal
 // element is read exactly once and each (u_k, v_k) element once per call.
+// More than kMaxBaby babies / diagonals: the caller runs chunks of <= 32 with
+// `accumulate` set after the first, into the same raised accumulators.
 #include "ck_internal.h"
 
 namespace ck {
@@ -50,8 +52,10 @@ __global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArg
     }
   }
   for (int j = 0; j < a.giant; ++j) {
-    const u64* d = a.diags + (long long)j * a.baby * rowN + off;
-    u64 yu = 0, yv = 0;
+    const long long dj = (long long)j * a.diag_stride;
+    u64* au = a.acc + (2LL * j) * rowN + off;
+    u64* av = a.acc + (2LL * j + 1) * rowN + off;
+    u64 yu = a.accumulate ? *au : 0, yv = a.accumulate ? *av : 0;
     // every diagonal of this giant group is requested before the first MAC
     constexpr int KL = MB < 16 ? MB : 16;
 #pragma unroll
@@ -59,7 +63,11 @@ __global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArg
     if (k1 >= a.baby) continue;
     u64 m[KL];
 #pragma unroll
-    for (int kk = 0; kk < KL; ++kk) m[kk] = k1 + kk < a.baby ? __ldg(d + (k1 + kk) * rowN) : 0;
+    for (int kk = 0; kk < KL; ++kk) {
+      const int k = k1 + kk;
+      m[kk] = k < a.baby ? __ldg(a.diag_ptrs ? a.diag_ptrs[dj + k] + off : a.diags + (dj + k) * rowN + off)
+                         : 0;
+    }
 #pragma unroll
     for (int k0 = k1; k0 < k1 + KL; k0 += 8) {
       if (k0 >= a.baby) continue;
@@ -80,13 +88,13 @@ __global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArg
       yv = addmod(yv, acc3_reduce(sv, P), P.q);
     }
     }
-    a.acc[(2LL * j) * rowN + off] = yu;
-    a.acc[(2LL * j + 1) * rowN + off] = yv;
+    *au = yu;
+    *av = yv;
   }
 }
 
 int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
-  if (a.baby < 1 || a.baby > kMaxBaby || a.giant < 1) return CK_ERR_ARG;
+  if (a.baby < 1 || a.baby > kMaxBaby || a.giant < 1 || a.diag_stride < a.baby) return CK_ERR_ARG;
   count_launches(1);
   const int n = 1 << a.logn;
 #define CK_DIAG(MB)                                                                    \

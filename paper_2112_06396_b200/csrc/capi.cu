@@ -135,6 +135,8 @@ struct ModDownTab {
   int* d_drop_prime = nullptr;
   int* d_keep_prime = nullptr;
   ulonglong2* d_pinv = nullptr;       // [P_drop]^-1 mod q_j per keep row
+  ulonglong2* d_dinv = nullptr;       // (product of the dropped CHAIN primes)^-1 mod q_j per keep
+                                      // row: pmodup(x) through this ModDown is x * d_dinv
 };
 
 struct LevelTab {
@@ -322,18 +324,23 @@ void build_moddown(ck_plan* p, ModDownTab& t, const std::vector<int>& keep,
     dscale[i] = sh2(mulmod_h(invmod_h(prod, qi), ninv, qi), qi);
     doff[i] = (long long)(drop_row0 + (int)i) << p->logn;
   }
-  std::vector<ulonglong2> pinv(keep.size());
+  std::vector<ulonglong2> pinv(keep.size()), dinv(keep.size());
   for (size_t j = 0; j < keep.size(); ++j) {
     const u64 qj = p->mod[keep[j]];
     u64 bp = 1 % qj;
     for (int d : drop) bp = mulmod_h(bp, p->mod[d] % qj, qj);
     pinv[j] = sh2(invmod_h(bp, qj), qj);
+    u64 bc = 1 % qj;
+    for (int d : drop)
+      if (d < p->L) bc = mulmod_h(bc, p->mod[d] % qj, qj);
+    dinv[j] = sh2(invmod_h(bc, qj), qj);
   }
   t.d_drop_scale = upload(p->allocs, dscale, err);
   t.d_drop_off = upload(p->allocs, doff, err);
   t.d_drop_prime = upload(p->allocs, drop, err);
   t.d_keep_prime = upload(p->allocs, keep, err);
   t.d_pinv = upload(p->allocs, pinv, err);
+  t.d_dinv = upload(p->allocs, dinv, err);
 }
 
 int build_level(ck_plan* p, int l) {
@@ -549,7 +556,30 @@ int modup_impl(const ck_plan* p, int l, const u64* a, u64* digits, u64* tmp, int
   return 0;
 }
 
-int kskip_impl(const ck_plan* p, int l, const u64* digits, const u64* kb, const u64* ka,
+// Switching keys of a batch: contiguous [B][dnum][L+K][N] blocks (base) or a
+// DEVICE array of B per-item block pointers (ptrs; SURVEY 8(b) key_ptrs[]).
+struct Keys {
+  const u64* b = nullptr;
+  const u64* a = nullptr;
+  const u64* const* bp = nullptr;
+  const u64* const* ap = nullptr;
+  bool shared = false;  // one key for the whole batch (relinearisation)
+  bool ok() const { return (b && a) || (bp && ap); }
+};
+Keys keys_block(const u64* b, const u64* a) {
+  Keys k;
+  k.b = b;
+  k.a = a;
+  return k;
+}
+Keys keys_ptrs(const u64* const* b, const u64* const* a, long long first = 0) {
+  Keys k;
+  k.bp = b ? b + first : nullptr;
+  k.ap = a ? a + first : nullptr;
+  return k;
+}
+
+int kskip_impl(const ck_plan* p, int l, const u64* digits, const Keys& keys,
                u64 gt, const u64* galois, u64* u, u64* v, long long uv_batch, int B,
                cudaStream_t st, bool shared_digits = false) {
   const LevelTab& t = p->lv[l];
@@ -558,10 +588,12 @@ int kskip_impl(const ck_plan* p, int l, const u64* digits, const u64* kb, const 
   a.digits = digits;
   a.digit_stride = (long long)t.R * N;
   a.digits_batch = shared_digits ? 0 : (long long)t.beta * t.R * N;
-  a.key_b = kb;
-  a.key_a = ka;
+  a.key_b = keys.b;
+  a.key_a = keys.a;
+  a.key_b_ptrs = keys.bp;
+  a.key_a_ptrs = keys.ap;
   a.key_digit_stride = (long long)(p->L + p->K) * N;
-  a.key_batch = (long long)p->key_digits * (p->L + p->K) * N;
+  a.key_batch = keys.shared ? 0 : (long long)p->key_digits * (p->L + p->K) * N;
   a.key_row = t.d_raised_prime;
   a.prime = t.d_raised_prime;
   a.pc = p->d_pc;
@@ -586,13 +618,27 @@ int moddown_core(const ck_plan* p, const ModDownTab& m, u64* x, long long xb, u6
                   false, st);
 }
 
-// Fused rotation key-switch (see fused.cu); 10 + beta launches per batch.
-int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add,
-                 const u64* kb, const u64* ka, u64 kgt, const u64* kgal, u64 egt,
-                 const u64* egal, u64* out_a, u64* out_b, const Ws& w, int B, cudaStream_t st) {
+// Fused key-switch of a batch (see fused.cu): ModUp (INTT row + column phase,
+// BC, forward column phase), ks_row (digit row phases + automorphism + KSKIP),
+// ModDown (INTT of the dropped rows, centered BC, forward column phase) and
+// md_row (forward row phase of the converted rows + epilogue); 10 launches.
+//   rotation (relin == nullptr): out = (u, v + automorph(b_add, egt/egal))
+//     after ModDown by P (ckks.py:655-681).
+//   relinearisation (relin = {b3, c3}, kgt = 1): u[l-1] += [P] b3[l-1],
+//     v[l-1] += [P] c3[l-1] before the merged ModDown by P*q_last; the kept rows'
+//     pmodup(b3), pmodup(c3) fold into the md_row epilogue as b3 * q_last^-1
+//     (exact mod q_j) -- new_mult's relinearisation (ckks.py:639-651).
+struct Relin {
+  const u64* b3;
+  const u64* c3;
+};
+int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add,
+                    const Keys& keys, u64 kgt, const u64* kgal, u64 egt, const u64* egal,
+                    const Relin* relin, u64* out_a, u64* out_b, const Ws& w, int B,
+                    cudaStream_t st) {
   const LevelTab& t = p->lv[level];
-  const ModDownTab& m = t.md[0];
-  const long long N = p->n, l = level, R = t.R;
+  const ModDownTab& m = t.md[relin ? 1 : 0];
+  const long long N = p->n, l = level, R = t.R, keep = m.keep;
   const long long dig_b = (long long)t.beta * R * N;
   // ---- ModUp: INTT of a (row then column phase, ihat*n^-1 folded), BC, fwd column phase
   CK_TRY(ntt_phase(p, w.tmp, t.d_chain_prime, nullptr, nullptr, level, B, l * N, true, 2, st,
@@ -612,16 +658,18 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   }
   CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs,
                      B, dig_b, false, 1, st));
-  // ---- row phase + automorph + KSKIP (+ INTT row phase of the special rows)
-  ck::KsRowArgs ka_;
+  // ---- row phase + automorph + KSKIP
+  ck::KsRowArgs ka_{};
   ka_.a_eval = a_src;
   ka_.a_batch = l * N;
   ka_.dig = w.dig;
   ka_.dig_batch = dig_b;
-  ka_.key_b = kb;
-  ka_.key_a = ka;
+  ka_.key_b = keys.b;
+  ka_.key_a = keys.a;
+  ka_.key_b_ptrs = keys.bp;
+  ka_.key_a_ptrs = keys.ap;
   ka_.key_digit_stride = (long long)(p->L + p->K) * N;
-  ka_.key_batch = (long long)p->key_digits * (p->L + p->K) * N;
+  ka_.key_batch = keys.shared ? 0 : (long long)p->key_digits * (p->L + p->K) * N;
   ka_.uv = w.uv;
   ka_.uv_batch = 2 * R * N;
   ka_.v_off = R * N;
@@ -641,18 +689,28 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ka_.logn = p->logn;
   ka_.key_prefetch = p->key_prefetch;
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
-  // ---- ModDown: INTT column phase of the special rows, centered BC, fwd column phase
+  if (relin) {
+    // pmodup (ckks.py:478-489) on the dropped chain row q_last: it feeds the BC
+    const int* lp = t.d_chain_prime + (l - 1);
+    const ulonglong2* pm = t.d_pmod + (l - 1);
+    CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + (l - 1) * N, 2 * R * N, w.uv + (l - 1) * N, 2 * R * N,
+                  relin->b3 + (l - 1) * N, l * N, nullptr, 0, lp, pm, 1, nullptr, 1, B, st));
+    CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + (R + l - 1) * N, 2 * R * N, w.uv + (R + l - 1) * N,
+                  2 * R * N, relin->c3 + (l - 1) * N, l * N, nullptr, 0, lp, pm, 1, nullptr, 1, B,
+                  st));
+  }
+  // ---- ModDown: INTT of the dropped rows, centered BC, fwd column phase
   CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
                    true, 0, st));
   {
     const ck::BconvArgs g1 = bconv_args(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv,
-                                        l * N, false);
+                                        keep * N, false);
     CK_TRY(ck::launch_bconv(g1, 2 * B, st));
-    CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, l * N, false,
+    CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, keep * N, false,
                      1, st));
   }
   // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
-  ck::MdRowArgs ma;
+  ck::MdRowArgs ma{};
   ma.prime = m.d_keep_prime;
   ma.pinv = m.d_pinv;
   ma.pc = p->d_pc;
@@ -661,20 +719,22 @@ int rotate_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add
   ma.x = w.uv;
   ma.x_batch = 2 * R * N;
   ma.conv = w.conv;
-  ma.conv_batch = 2 * l * N;
-  ma.addend = b_add;
+  ma.conv_batch = 2 * keep * N;
+  ma.addend = relin ? relin->c3 : b_add;
+  ma.addend_u = relin ? relin->b3 : nullptr;
+  ma.add_scale = relin ? m.d_dinv : nullptr;
   ma.addend_batch = l * N;
   ma.out = out_a;
-  ma.out_batch = l * N;
-  ma.galois = egal;
-  ma.galois_t = egt;
+  ma.out_batch = keep * N;
+  ma.galois = relin ? nullptr : egal;
+  ma.galois_t = relin ? 1 : egt;
   ma.pair = 1;
   ma.x_w = R * N;
-  ma.conv_w = l * N;
+  ma.conv_w = keep * N;
   ma.out2 = out_b;
   ma.lazy = 1;
-  for (int k = 0; k < level; ++k) ma.lazy &= p->mod[k] < ((u64)1 << 59) ? 1 : 0;
-  return ck::launch_md_row(ma, level, B, st);
+  for (int k = 0; k < keep; ++k) ma.lazy &= p->mod[k] < ((u64)1 << 59) ? 1 : 0;
+  return ck::launch_md_row(ma, (int)keep, B, st);
 }
 
 }  // namespace
@@ -826,10 +886,11 @@ int ck_poly_op(const ck_plan* p, int op, uint64_t* out_, const uint64_t* x_, con
   u64* out = (u64*)out_;
   const u64* x = (const u64*)x_;
   const u64* y = (const u64*)y_;
-  if (!p || !out || !x || !prime_idx || op < 0 || op > 5) return CK_ERR_ARG;
+  if (!p || !out || !x || !prime_idx || op < 0 || op > 6) return CK_ERR_ARG;
   if ((op <= 2) && !y) return CK_ERR_ARG;
-  if (op == 4 && !cst) return CK_ERR_ARG;
-  return ew_run(p, op, out, 0, x, 0, y, 0, nullptr, 0, prime_idx, (const ulonglong2*)cst, 1,
+  if ((op == 4 || op == 6) && !cst) return CK_ERR_ARG;
+  return ew_run(p, op == 6 ? ck::EW_ADDC : op, out, 0, x, 0, y, 0, nullptr, 0, prime_idx,
+                (const ulonglong2*)cst, 1,
                 nullptr, rows, 1, (cudaStream_t)stream);
 }
 
@@ -898,7 +959,7 @@ int ck_kskip(const ck_plan* p, const uint64_t* digits_, const uint64_t* key_b_,
       (galois_t & 1) == 0)
     return CK_ERR_ARG;
   const long long ub = (long long)p->lv[level].R * p->n;
-  return kskip_impl(p, level, digits, key_b, key_a, galois_t, galois, u, v, ub, batch,
+  return kskip_impl(p, level, digits, keys_block(key_b, key_a), galois_t, galois, u, v, ub, batch,
                     (cudaStream_t)stream);
 }
 
@@ -923,18 +984,17 @@ int ck_moddown(const ck_plan* p, uint64_t* x_, int level, int merged, uint64_t* 
                 batch, st);
 }
 
-int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
-              const uint64_t* key_a_, int level, uint64_t galois_t, const uint64_t* galois_,
-              int mode, uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, int batch,
-              ck_stream stream) {
-  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *key_b = (const u64*)key_b_,
-            *key_a = (const u64*)key_a_, *galois = (const u64*)galois_;
-  u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *workspace = (u64*)workspace_;
-  if (!level_ok(p, level) || !a || !b || !key_b || !key_a || !out_a || !out_b || !workspace ||
+}  // extern "C"
+
+namespace {
+// rotation / conjugation key-switch of a batch (ck_rotate; giant steps of ck_bsgs)
+int rotate_impl(const ck_plan* p, const u64* a, const u64* b, const Keys& keys, int level,
+                uint64_t galois_t, const u64* galois, int mode, u64* out_a, u64* out_b,
+                u64* workspace, int batch, cudaStream_t st) {
+  if (!level_ok(p, level) || !a || !b || !keys.ok() || !out_a || !out_b || !workspace ||
       batch < 1 || (mode != 0 && mode != 1) || (galois_t & 1) == 0 || p->K < 1)
     return CK_ERR_ARG;
   if (mode == 1 && galois) return CK_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
   const LevelTab& t = p->lv[level];
   const long long N = p->n, l = level, R = t.R;
   const Ws w = ws_layout(p, level, batch, workspace);
@@ -957,13 +1017,12 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
   }
   if (ck::fused_supported(p->logn) && p->fused) {
     const u64* egal = mode == 1 ? nullptr : galois;
-    return rotate_fused(p, level, a_src, b_add, key_b, key_a, kgt, kgal, egt, egal, out_a, out_b,
-                        w, batch, st);
+    return keyswitch_fused(p, level, a_src, b_add, keys, kgt, kgal, egt, egal, nullptr, out_a,
+                           out_b, w, batch, st);
   }
   CK_TRY(modup_impl(p, level, a_src, w.dig, w.tmp, batch, st));
   // uv: [B][2][R][N]
-  CK_TRY(kskip_impl(p, level, w.dig, key_b, key_a, kgt, kgal, w.uv, w.uv + R * N, 2 * R * N,
-                    batch, st));
+  CK_TRY(kskip_impl(p, level, w.dig, keys, kgt, kgal, w.uv, w.uv + R * N, 2 * R * N, batch, st));
   const ModDownTab& m = t.md[0];
   CK_TRY(moddown_core(p, m, w.uv, R * N, w.conv, 2 * batch, st));
   // conv: [B][2][l][N]
@@ -973,45 +1032,61 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
                 2 * l * N, b_add, l * N, m.d_keep_prime, m.d_pinv, egt, mode == 1 ? nullptr : galois,
                 level, batch, st);
 }
+}  // namespace
 
-size_t ck_relin_workspace_bytes(const ck_plan* p, int level) {
-  if (!level_ok(p, level) || level < 2) return 0;
-  const LevelTab& t = p->lv[level];
-  const size_t rows = (size_t)t.beta * t.R + 2 * (size_t)t.R + (size_t)level;
-  return rows * p->n * sizeof(u64) + ck_workspace_bytes(p, level, 1);
+extern "C" {
+
+int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
+              const uint64_t* key_a_, int level, uint64_t galois_t, const uint64_t* galois_,
+              int mode, uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, int batch,
+              ck_stream stream) {
+  return rotate_impl(p, (const u64*)a_, (const u64*)b_,
+                     keys_block((const u64*)key_b_, (const u64*)key_a_), level, galois_t,
+                     (const u64*)galois_, mode, (u64*)out_a_, (u64*)out_b_, (u64*)workspace_,
+                     batch, (cudaStream_t)stream);
+}
+
+size_t ck_relin_workspace_bytes(const ck_plan* p, int level, int batch) {
+  if (!level_ok(p, level) || level < 2 || batch < 1) return 0;
+  return ck_workspace_bytes(p, level, batch);
 }
 
 int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const uint64_t* c3_,
              const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a_,
-             uint64_t* out_b_, uint64_t* workspace_, ck_stream stream) {
+             uint64_t* out_b_, uint64_t* workspace_, int batch, ck_stream stream) {
   const u64 *a3 = (const u64*)a3_, *b3 = (const u64*)b3_, *c3 = (const u64*)c3_;
   u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
   if (!level_ok(p, level) || level < 2 || !a3 || !b3 || !c3 || !key_b || !key_a || !out_a ||
-      !out_b || !ws || p->K < 1)
+      !out_b || !ws || batch < 1 || p->K < 1)
     return CK_ERR_ARG;
   const LevelTab& t = p->lv[level];
   if (!t.md[1].valid) return CK_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const long long N = p->n, R = t.R, l = level;
-  u64* dig = ws;                       // [beta][R][N]
-  u64* uv = dig + (long long)t.beta * R * N;  // u [R][N], v [R][N]
-  u64* tmp = uv + 2 * R * N;           // [l][N]
-  u64* w2 = tmp + l * N;               // ck_workspace_bytes(level, 1)
-  CK_TRY(ck_modup(p, a3_, level, (uint64_t*)dig, (uint64_t*)w2, 1, stream));
-  CK_TRY(ck_kskip(p, (const uint64_t*)dig, key_b, key_a, level, 1, nullptr, (uint64_t*)uv,
-                  (uint64_t*)(uv + R * N), 1, stream));
-  // pmodup (ckks.py:478-489): chain rows += [P]_q * x, special rows += 0
-  for (int half = 0; half < 2; ++half) {
-    u64* dst = uv + half * R * N;
-    CK_TRY(ew_run(p, ck::EW_MULC, tmp, 0, half ? c3 : b3, 0, nullptr, 0, nullptr, 0,
-                  t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, 1, st));
-    CK_TRY(ew_run(p, ck::EW_ADD, dst, 0, dst, 0, tmp, 0, nullptr, 0, t.d_chain_prime, nullptr, 1,
-                  nullptr, (int)l, 1, st));
+  const Ws w = ws_layout(p, level, batch, ws);
+  Keys keys = keys_block((const u64*)key_b, (const u64*)key_a);
+  keys.shared = true;  // one relinearisation key for the whole batch
+  if (ck::fused_supported(p->logn) && p->fused) {
+    const Relin rl{b3, c3};
+    return keyswitch_fused(p, level, a3, nullptr, keys, 1, nullptr, 1, nullptr, &rl, out_a, out_b,
+                           w, batch, st);
   }
-  // ModDown by P * q_last (ckks.py:643-651)
-  CK_TRY(ck_moddown(p, (uint64_t*)uv, level, 1, out_a_, nullptr, 1, (uint64_t*)w2, 1, stream));
-  return ck_moddown(p, (uint64_t*)(uv + R * N), level, 1, out_b_, nullptr, 1, (uint64_t*)w2, 1,
-                    stream);
+  // unfused pipeline (small rings): ModUp, relin KSKIP, pmodup add, ModDown by P * q_last
+  const ModDownTab& m = t.md[1];
+  CK_TRY(modup_impl(p, level, a3, w.dig, w.tmp, batch, st));
+  CK_TRY(kskip_impl(p, level, w.dig, keys, 1, nullptr, w.uv, w.uv + R * N, 2 * R * N, batch, st));
+  // pmodup (ckks.py:478-489): chain rows += [P]_q * x, special rows += 0
+  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv, 2 * R * N, w.uv, 2 * R * N, b3, l * N, nullptr, 0,
+                t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, batch, st));
+  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + R * N, 2 * R * N, w.uv + R * N, 2 * R * N, c3, l * N,
+                nullptr, 0, t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, batch, st));
+  // ModDown pair by P * q_last (ckks.py:643-651), u and v as one batch of 2B
+  CK_TRY(moddown_core(p, m, w.uv, R * N, w.conv, 2 * batch, st));
+  const long long lo = m.keep;
+  CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, lo * N, w.uv, 2 * R * N, w.conv, 2 * lo * N, nullptr, 0,
+                m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, batch, st));
+  return ew_run(p, ck::EW_MODDOWN, out_b, lo * N, w.uv + R * N, 2 * R * N, w.conv + lo * N,
+                2 * lo * N, nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, batch, st);
 }
 
 size_t ck_hrotate_workspace_bytes(const ck_plan* p, int level, int n_rot) {
@@ -1022,13 +1097,14 @@ size_t ck_hrotate_workspace_bytes(const ck_plan* p, int level, int n_rot) {
   return (size_t)rows * p->n * sizeof(u64);
 }
 
-int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
-               const uint64_t* key_a_, const uint64_t* galois_, int level, int n_rot,
-               uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, ck_stream stream) {
-  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *kb = (const u64*)key_b_,
-            *ka = (const u64*)key_a_, *gal = (const u64*)galois_;
+int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
+               const uint64_t* const* key_b_, const uint64_t* const* key_a_,
+               const uint64_t* galois_, int level, int n_rot, uint64_t* out_a_, uint64_t* out_b_,
+               uint64_t* workspace_, ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *gal = (const u64*)galois_;
+  const Keys keys = keys_ptrs((const u64* const*)key_b_, (const u64* const*)key_a_);
   u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
-  if (!level_ok(p, level) || !a || !b || !kb || !ka || !gal || !out_a || !out_b || !ws ||
+  if (!level_ok(p, level) || !a || !b || !keys.ok() || !gal || !out_a || !out_b || !ws ||
       n_rot < 1 || p->K < 1)
     return CK_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1042,8 +1118,8 @@ int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const u
   // one shared ModUp (the hoisting, ckks.py:660), digits in evaluation form
   CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
   // every rotation's KSKIP in one launch: digits shared, automorphism folded
-  // into the gather, per-rotation key and Galois element
-  CK_TRY(kskip_impl(p, level, dig, kb, ka, 1, gal, uv, uv + R * N, 2 * R * N, n_rot, st, true));
+  // into the gather, per-rotation key (pointer array) and Galois element
+  CK_TRY(kskip_impl(p, level, dig, keys, 1, gal, uv, uv + R * N, 2 * R * N, n_rot, st, true));
   // ModDown pair of every rotation (ckks.py:664-666): b is shared, gathered
   // with each rotation's Galois element
   CK_TRY(moddown_core(p, m, uv, R * N, conv, 2 * n_rot, st));
@@ -1053,61 +1129,76 @@ int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const u
                 0, m.d_keep_prime, m.d_pinv, 1, gal, level, n_rot, st);
 }
 
+// diagonals / baby steps per diag_mac launch (bsgs.cu kMaxBaby); more run in chunks
+constexpr int kDiagChunk = 32;
+
 size_t ck_pt_matvec_workspace_bytes(const ck_plan* p, int level, int n_diag) {
   if (!level_ok(p, level) || level < 2 || n_diag < 1 || p->K < 1) return 0;
   const LevelTab& t = p->lv[level];
-  const long long rows = (long long)t.beta * t.R + level + (long long)n_diag * 2 * t.R +
-                         2LL * t.R + 2LL * level;
+  const long long chunk = std::min(n_diag, kDiagChunk);
+  const long long rows = (long long)t.beta * t.R + level + chunk * 2 * t.R + 2LL * t.R +
+                         2LL * level;
   return (size_t)rows * p->n * sizeof(u64);
 }
 
-int ck_pt_matvec(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
-                 const uint64_t* key_a_, const uint64_t* galois_, const uint64_t* diags_,
-                 int level, int n_rot, int has_identity, uint64_t* out_a_, uint64_t* out_b_,
-                 uint64_t* workspace_, ck_stream stream) {
-  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *kb = (const u64*)key_b_,
-            *ka = (const u64*)key_a_, *gal = (const u64*)galois_, *diags = (const u64*)diags_;
+int ck_pt_matvec(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
+                 const uint64_t* const* key_b_, const uint64_t* const* key_a_,
+                 const uint64_t* galois_, const uint64_t* const* diags_, int level, int n_rot,
+                 int has_identity, uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_,
+                 ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *gal = (const u64*)galois_;
+  const u64* const* diags = (const u64* const*)diags_;
+  const Keys keys = keys_ptrs((const u64* const*)key_b_, (const u64* const*)key_a_);
   u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
   const int nd = n_rot + (has_identity ? 1 : 0);
   if (!level_ok(p, level) || level < 2 || !a || !b || !diags || !gal || !out_a || !out_b ||
-      !ws || n_rot < 0 || nd < 1 || nd > 32 || p->K < 1 || (n_rot > 0 && (!kb || !ka)))
+      !ws || n_rot < 0 || nd < 1 || p->K < 1 || (n_rot > 0 && !keys.ok()))
     return CK_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const LevelTab& t = p->lv[level];
   const ModDownTab& m = t.md[1];
   const long long N = p->n, l = level, R = t.R, lo = l - 1;
+  const int chunk = std::min(nd, kDiagChunk);
   u64* dig = ws;
   u64* tmp = dig + (long long)t.beta * R * N;
-  u64* uvb = tmp + l * N;                      // [nd][2][R][N]
-  u64* acc = uvb + (long long)nd * 2 * R * N;  // [2][R][N]
-  u64* conv = acc + 2 * R * N;                 // [2][l][N]
-  if (n_rot > 0) {
-    CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
-    CK_TRY(kskip_impl(p, level, dig, kb, ka, 1, gal, uvb, uvb + R * N, 2 * R * N, n_rot, st, true));
+  u64* uvb = tmp + l * N;                         // [chunk][2][R][N]
+  u64* acc = uvb + (long long)chunk * 2 * R * N;  // [2][R][N]
+  u64* conv = acc + 2 * R * N;                    // [2][l][N]
+  if (n_rot > 0) CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
+  // any number of diagonals (ckks.py:699-711): chunks of <= 32 accumulate into
+  // the same raised accumulators before the single merged ModDown
+  for (int c0 = 0; c0 < nd; c0 += chunk) {
+    const int cnt = std::min(chunk, nd - c0);
+    const int nrot_c = std::max(0, std::min(cnt, n_rot - c0));
+    if (nrot_c > 0)
+      CK_TRY(kskip_impl(p, level, dig, keys_ptrs(keys.bp, keys.ap, c0), 1, gal + c0, uvb,
+                        uvb + R * N, 2 * R * N, nrot_c, st, true));
+    if (nrot_c < cnt) {
+      // identity diagonal (ckks.py:701-704): u = pmodup(a), v = 0 (+ P b added by
+      // the MAC kernel with Galois element 1 -> pmodup(b))
+      u64* ui = uvb + (long long)nrot_c * 2 * R * N;
+      CK_TRY((int)cudaMemsetAsync(ui, 0, sizeof(u64) * 2 * R * N, st));
+      CK_TRY(ew_run(p, ck::EW_MULC, ui, 0, a, 0, nullptr, 0, nullptr, 0, t.d_chain_prime,
+                    t.d_pmod, 1, nullptr, level, 1, st));
+    }
+    ck::DiagArgs da{};
+    da.uv = uvb;
+    da.b = b;
+    da.diag_ptrs = diags + c0;
+    da.diag_stride = cnt;
+    da.accumulate = c0 > 0;
+    da.acc = acc;
+    da.galois = gal + c0;  // identity's element is 1 (set by the caller)
+    da.prime = t.d_raised_prime;
+    da.pmod = t.d_pmod;
+    da.pc = p->d_pc;
+    da.baby = cnt;
+    da.giant = 1;
+    da.R = (int)R;
+    da.l = level;
+    da.logn = p->logn;
+    CK_TRY(ck::launch_diag_mac(da, st));
   }
-  if (has_identity) {
-    // identity diagonal (ckks.py:701-704): u = pmodup(a), v = 0 (+ P b added by
-    // the MAC kernel with Galois element 1 -> pmodup(b))
-    u64* ui = uvb + (long long)n_rot * 2 * R * N;
-    CK_TRY((int)cudaMemsetAsync(ui, 0, sizeof(u64) * 2 * R * N, st));
-    CK_TRY(ew_run(p, ck::EW_MULC, ui, 0, a, 0, nullptr, 0, nullptr, 0, t.d_chain_prime, t.d_pmod,
-                  1, nullptr, level, 1, st));
-  }
-  ck::DiagArgs da;
-  da.uv = uvb;
-  da.b = b;
-  da.diags = diags;
-  da.acc = acc;
-  da.galois = gal;  // [nd]: identity's element is 1 (set by the caller)
-  da.prime = t.d_raised_prime;
-  da.pmod = t.d_pmod;
-  da.pc = p->d_pc;
-  da.baby = nd;
-  da.giant = 1;
-  da.R = (int)R;
-  da.l = level;
-  da.logn = p->logn;
-  CK_TRY(ck::launch_diag_mac(da, st));
   // one merged ModDown pair by P * q_last (ckks.py:712-717)
   CK_TRY(moddown_core(p, m, acc, R * N, conv, 2, st));
   CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, 0, acc, 0, conv, 0, nullptr, 0, m.d_keep_prime, m.d_pinv,
@@ -1120,34 +1211,37 @@ size_t ck_bsgs_workspace_bytes(const ck_plan* p, int level, int baby, int giant)
   if (!level_ok(p, level) || level < 2 || baby < 1 || giant < 1) return 0;
   const LevelTab& t = p->lv[level];
   const long long N = p->n, l = level, R = t.R;
-  const long long rows = (long long)t.beta * R + l + (long long)baby * 2 * R +
+  const long long chunk = std::min(baby, kDiagChunk);
+  const long long rows = (long long)t.beta * R + l + chunk * 2 * R +
                          (long long)giant * 2 * R + (long long)giant * 2 * l +
                          (long long)giant * 4 * (l - 1);
   return (size_t)rows * N * sizeof(u64) + ck_workspace_bytes(p, level - 1, giant);
 }
 
-int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* bkb_,
-            const uint64_t* bka_, const uint64_t* gkb_, const uint64_t* gka_,
-            const uint64_t* diags_, const uint64_t* baby_galois_, const uint64_t* giant_galois_,
-            int level, int baby, int giant, uint64_t* out_a_, uint64_t* out_b_,
-            uint64_t* workspace_, ck_stream stream) {
-  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *bkb = (const u64*)bkb_,
-            *bka = (const u64*)bka_, *gkb = (const u64*)gkb_, *gka = (const u64*)gka_,
-            *diags = (const u64*)diags_, *bgal = (const u64*)baby_galois_,
+int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
+            const uint64_t* const* bkb_, const uint64_t* const* bka_,
+            const uint64_t* const* gkb_, const uint64_t* const* gka_,
+            const uint64_t* const* diags_, const uint64_t* baby_galois_,
+            const uint64_t* giant_galois_, int level, int baby, int giant, uint64_t* out_a_,
+            uint64_t* out_b_, uint64_t* workspace_, ck_stream stream) {
+  const u64 *a = (const u64*)a_, *b = (const u64*)b_, *bgal = (const u64*)baby_galois_,
             *ggal = (const u64*)giant_galois_;
+  const u64* const* diags = (const u64* const*)diags_;
+  const Keys bkeys = keys_ptrs((const u64* const*)bkb_, (const u64* const*)bka_);
+  const Keys gkeys = keys_ptrs((const u64* const*)gkb_, (const u64* const*)gka_);
   u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
-  if (!level_ok(p, level) || level < 2 || !a || !b || !bkb || !bka || !gkb || !gka || !diags ||
-      !bgal || !ggal || !out_a || !out_b || !ws || baby < 1 || baby > 32 || giant < 1 ||
-      p->K < 1)
+  if (!level_ok(p, level) || level < 2 || !a || !b || !bkeys.ok() || !gkeys.ok() || !diags ||
+      !bgal || !ggal || !out_a || !out_b || !ws || baby < 1 || giant < 1 || p->K < 1)
     return CK_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const LevelTab& t = p->lv[level];
   const ModDownTab& m = t.md[1];
   const long long N = p->n, l = level, R = t.R, lo = l - 1;
+  const int chunk = std::min(baby, kDiagChunk);
   u64* dig = ws;
   u64* tmp = dig + (long long)t.beta * R * N;
-  u64* uvb = tmp + l * N;                       // [baby][2][R][N]
-  u64* acc = uvb + (long long)baby * 2 * R * N; // [giant][2][R][N]
+  u64* uvb = tmp + l * N;                        // [chunk][2][R][N]
+  u64* acc = uvb + (long long)chunk * 2 * R * N; // [giant][2][R][N]
   u64* conv = acc + (long long)giant * 2 * R * N;
   u64* ga = conv + (long long)giant * 2 * l * N; // [giant][l-1][N]
   u64* gb = ga + (long long)giant * lo * N;
@@ -1156,25 +1250,31 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint
   u64* rws = rb + (long long)giant * lo * N;
   // 1. one shared ModUp (hoisting)
   CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
-  // 2. all baby KSKIPs in one launch: digits shared, per-baby key and Galois element
-  CK_TRY(kskip_impl(p, level, dig, bkb, bka, 1, bgal, uvb, uvb + R * N, 2 * R * N, baby, st,
-                    true));
-  // 3. diagonal MAC into giant accumulators (pmodup(automorph(b)) folded in)
-  ck::DiagArgs da;
-  da.uv = uvb;
-  da.b = b;
-  da.diags = diags;
-  da.acc = acc;
-  da.galois = bgal;
-  da.prime = t.d_raised_prime;
-  da.pmod = t.d_pmod;
-  da.pc = p->d_pc;
-  da.baby = baby;
-  da.giant = giant;
-  da.R = (int)R;
-  da.l = level;
-  da.logn = p->logn;
-  CK_TRY(ck::launch_diag_mac(da, st));
+  for (int c0 = 0; c0 < baby; c0 += chunk) {
+    const int cnt = std::min(chunk, baby - c0);
+    // 2. the chunk's baby KSKIPs in one launch: digits shared, per-baby key and Galois element
+    CK_TRY(kskip_impl(p, level, dig, keys_ptrs(bkeys.bp, bkeys.ap, c0), 1, bgal + c0, uvb,
+                      uvb + R * N, 2 * R * N, cnt, st, true));
+    // 3. diagonal MAC into giant accumulators (pmodup(automorph(b)) folded in);
+    //    chunks after the first accumulate
+    ck::DiagArgs da{};
+    da.uv = uvb;
+    da.b = b;
+    da.diag_ptrs = diags + c0;
+    da.diag_stride = baby;
+    da.accumulate = c0 > 0;
+    da.acc = acc;
+    da.galois = bgal + c0;
+    da.prime = t.d_raised_prime;
+    da.pmod = t.d_pmod;
+    da.pc = p->d_pc;
+    da.baby = cnt;
+    da.giant = giant;
+    da.R = (int)R;
+    da.l = level;
+    da.logn = p->logn;
+    CK_TRY(ck::launch_diag_mac(da, st));
+  }
   // 4. merged ModDown (P * q_last) of every accumulator -> level l-1
   CK_TRY(moddown_core(p, m, acc, R * N, conv, 2 * giant, st));
   CK_TRY(ew_run(p, ck::EW_MODDOWN, ga, lo * N, acc, 2 * R * N, conv, 2 * lo * N, nullptr, 0,
@@ -1182,8 +1282,7 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint
   CK_TRY(ew_run(p, ck::EW_MODDOWN, gb, lo * N, acc + R * N, 2 * R * N, conv + lo * N, 2 * lo * N,
                 nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
   // 5. giant rotations at l-1, batched
-  CK_TRY(ck_rotate(p, (const uint64_t*)ga, (const uint64_t*)gb, gkb_, gka_, (int)lo, 1,
-                   giant_galois_, 0, (uint64_t*)ra, (uint64_t*)rb, (uint64_t*)rws, giant, stream));
+  CK_TRY(rotate_impl(p, ga, gb, gkeys, (int)lo, 1, ggal, 0, ra, rb, rws, giant, st));
   // 6. sum of the rotated giants
   const int* kp = p->lv[lo].d_chain_prime;
   if (giant == 1) {

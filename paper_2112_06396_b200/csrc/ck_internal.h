@@ -75,6 +75,8 @@ struct KsRowArgs {
   const u64* key_b;
   const u64* key_a;
   long long key_digit_stride, key_batch;
+  const u64* const* key_b_ptrs; // nullable: per-item key blocks [B] (overrides key_b + b*key_batch)
+  const u64* const* key_a_ptrs;
   u64* uv;                      // u at uv + i*N, v at uv + v_off + i*N (per batch item)
   long long uv_batch, v_off;
   const int* prime;             // [R] raised prime index (== full-basis key row)
@@ -88,14 +90,23 @@ struct KsRowArgs {
   int key_prefetch;             // bulk L2 prefetch of the first k/8 of each key tile at kernel start
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
+#ifdef __CUDACC__
+// base of batch item b's key block: pointer array when given, else base + b * stride
+__device__ __forceinline__ const u64* key_block(const u64* base, const u64* const* ptrs,
+                                                long long stride, long long b) {
+  return ptrs ? ptrs[b] : base + b * stride;
+}
+#endif
 
 struct MdRowArgs {
   const u64* x;                 // [B][..][N] raised-basis rows (kept rows j = 0..keep)
   long long x_batch;
   const u64* conv;              // [B][keep][N] converted rows after the column phase
   long long conv_batch;
-  const u64* addend;            // nullable [B][keep][N], gathered with galois
+  const u64* addend;            // nullable [B][keep][N], gathered with galois (v / out2 only)
+  const u64* addend_u;          // nullable [B][keep][N], pair mode's first polynomial (u / out)
   long long addend_batch;
+  const ulonglong2* add_scale;  // nullable [keep] Shoup pairs: addends multiplied by them
   u64* out;
   long long out_batch;
   const int* prime;             // [keep]
@@ -119,6 +130,9 @@ struct DiagArgs {
   const u64* uv;                // [baby][2][R][N]
   const u64* b;                 // [l][N]
   const u64* diags;             // [giant][baby][R][N]
+  const u64* const* diag_ptrs;  // nullable: [giant][baby] per-diagonal [R][N] rows (overrides diags)
+  int diag_stride;              // diag_ptrs row stride (entries between giant groups)
+  int accumulate;               // 1: acc += (chunks of > 32 diagonals / babies)
   u64* acc;                     // [giant][2][R][N]
   const u64* galois;            // [baby] device
   const int* prime;             // [R]
@@ -167,6 +181,8 @@ struct KskipArgs {
   const u64* key_a;
   long long key_digit_stride;   // elements between key digits (LK*N)
   long long key_batch;
+  const u64* const* key_b_ptrs; // nullable: per-item key blocks [B] (overrides key_b + b*key_batch)
+  const u64* const* key_a_ptrs;
   const int* key_row;           // [R] full-basis row of raised row i
   const int* prime;             // [R] prime index of raised row i
   const PrimeConst* pc;
@@ -181,7 +197,8 @@ int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st);
 
 // Elementwise ops over limb rows.
 enum EwOp { EW_ADD = 0, EW_SUB = 1, EW_MUL = 2, EW_NEG = 3, EW_MULC = 4, EW_COPY = 5,
-            EW_MODDOWN = 6, EW_AUTOMORPH = 7, EW_SUMN = 8 };
+            EW_MODDOWN = 6, EW_AUTOMORPH = 7, EW_SUMN = 8, EW_ADDC = 9,
+            EW_ADDMULC = 10 };
 struct EwArgs {
   u64* out;
   const u64* x;

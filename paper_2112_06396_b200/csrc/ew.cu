@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(kEwThreads) ew_kernel(EwArgs a) {
     case EW_MUL: r = mulmod(x[k], y[k], P); break;
     case EW_NEG: { const u64 v = x[k]; r = v ? q - v : 0; } break;
     case EW_MULC: { const ulonglong2 c = a.cst[row]; r = shoup(x[k], c.x, c.y, q); } break;
+    case EW_ADDC: r = addmod(x[k], a.cst[row].x, q); break;
+    case EW_ADDMULC: { const ulonglong2 c = a.cst[row]; r = addmod(x[k], shoup(y[k], c.x, c.y, q), q); } break;
     case EW_COPY: r = x[k]; break;
     case EW_AUTOMORPH:
       r = gt == 1 ? x[k] : x[automorph_src((u32)k, (u32)gt, a.logn)];

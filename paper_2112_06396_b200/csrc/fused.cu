@@ -102,8 +102,9 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   // key_prefetch = k: prefetch the first k/8 of each key row-tile (k = 8: all)
   if (a.key_prefetch && threadIdx.x < 2 * beta) {
     const int d = threadIdx.x >> 1;
-    const u64* kbase = (threadIdx.x & 1) ? a.key_a : a.key_b;
-    prefetch_l2(kbase + b * a.key_batch + d * a.key_digit_stride + ((long long)prime << LOGN) +
+    const u64* kbase = (threadIdx.x & 1) ? key_block(a.key_a, a.key_a_ptrs, a.key_batch, b)
+                                         : key_block(a.key_b, a.key_b_ptrs, a.key_batch, b);
+    prefetch_l2(kbase + d * a.key_digit_stride + ((long long)prime << LOGN) +
                     ((long long)blockIdx.x * F::TR << P2),
                 (F::TR * F::S * 8 / 8) * min(a.key_prefetch, 8));
   }
@@ -169,8 +170,8 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   // vectors and every warp instruction covers 512 contiguous bytes.
   // Output column c of row r reads column pi_r(c) of row sigma(r).
   const long long tile0 = (long long)blockIdx.x * F::TR << P2;
-  const u64* ka = a.key_a + b * a.key_batch + ((long long)prime << LOGN) + tile0;
-  const u64* kb = a.key_b + b * a.key_batch + ((long long)prime << LOGN) + tile0;
+  const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
+  const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
   u64* ubase = a.uv + b * a.uv_batch + ((long long)i << LOGN);
   u64* uo = ubase + ((long long)r << P2);
   u64* vo = uo + a.v_off;
@@ -316,10 +317,13 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
     o[k] = lazy ? shoup(x[c] + (q << 4) - srow[sidx(c)], pinv.x, pinv.y, q)
                 : shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
   }
-  if (a.addend && w) {
+  const u64* addp = w ? a.addend : a.addend_u;
+  if (addp) {
     const u64 t = a.galois ? a.galois[b] : a.galois_t;
     const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
-    const u64* add = a.addend + b * a.addend_batch + ((long long)j << LOGN) + ((long long)sr << P2);
+    const u64* add = addp + b * a.addend_batch + ((long long)j << LOGN) + ((long long)sr << P2);
+    // relinearisation: pmodup(b3) through the merged ModDown is b3 * q_last^-1
+    const ulonglong2 asc = a.add_scale ? a.add_scale[j] : make_ulonglong2(0, 0);
     u64 z[kE];
 #pragma unroll
     for (int k = 0; k < kE; ++k) z[k] = add[sub_index<P2, 0, false>(g, k)];
@@ -331,7 +335,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
       const int c = sub_index<P2, 0, false>(g, k);
       const int sc = t == 1 ? c
                             : (int)(automorph_src(((u32)r << P2) + c, (u32)t, LOGN) & (F::S - 1));
-      o[k] = addmod(o[k], srow[sidx(sc)], q);
+      const u64 z = srow[sidx(sc)];
+      o[k] = addmod(o[k], a.add_scale ? shoup(z, asc.x, asc.y, q) : z, q);
     }
   }
   u64* out = (a.pair && w ? a.out2 : a.out) + b * a.out_batch + ((long long)j << LOGN) +

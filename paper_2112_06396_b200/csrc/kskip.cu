@@ -21,7 +21,7 @@ CK_HD int ks_row_bits(int logn) { return logn < 9 ? logn : 9; }
 constexpr int kKsThreads = 256;
 constexpr int kKsMaxBeta = 8;
 
-// grid = (N / TILE, rows, batch); TILE = 512 elements (or N if smaller).
+// grid = (batch, N / TILE, rows); TILE = 512 elements (or N if smaller).
 // BETA > 0: compile-time digit count, every key element of a thread's
 // coefficients is requested before the first multiply (the kernel streams
 // keys, so memory-level parallelism is what matters); BETA = 0: runtime.
@@ -41,8 +41,8 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
   const u64 t = a.galois ? a.galois[bz] : a.galois_t;
   const long long tile0 = (long long)blockIdx.y * TILE;
   const int krow = a.key_row[i];
-  const u64* kb = a.key_b + bz * a.key_batch + ((long long)krow << logn);
-  const u64* ka = a.key_a + bz * a.key_batch + ((long long)krow << logn);
+  const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, bz) + ((long long)krow << logn);
+  const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, bz) + ((long long)krow << logn);
   const u64* dig = a.digits + bz * a.digits_batch + ((long long)i << logn);
   // stage the gathered digit rows: for each storage row in the tile load the
   // source row perm maps it to

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -68,7 +69,6 @@ class Plan:
         self.h = h
         self._lib = lib
         self._idx: dict[tuple, torch.Tensor] = {}
-        self._ws: dict[tuple, torch.Tensor] = {}
         self._bc: dict[tuple, C.c_void_p] = {}
         self._lock = threading.Lock()
         info = (C.c_int64 * 5)()
@@ -92,16 +92,14 @@ class Plan:
             self._idx[key] = t
         return t
 
-    def workspace(self, level: int, batch: int, tag: str = "") -> torch.Tensor:
-        key = (level, batch, tag)
-        t = self._ws.get(key)
-        if t is None:
-            nbytes = self._lib.ck_workspace_bytes(self.h, level, batch)
-            if nbytes == 0:
-                raise AssertionError(f"bad level {level}")
-            t = torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
-            self._ws[key] = t
-        return t
+    def workspace(self, level: int, batch: int) -> torch.Tensor:
+        """Scratch for one ck_rotate / ck_modup / ck_moddown call, allocated per
+        call from torch's stream-ordered caching allocator: concurrent callers
+        on different streams or threads never share it."""
+        nbytes = self._lib.ck_workspace_bytes(self.h, level, batch)
+        if nbytes == 0:
+            raise AssertionError(f"bad level {level}")
+        return torch.empty(nbytes // 8, dtype=torch.uint64, device="cuda")
 
     def bconv(self, src, dst, centered: bool) -> C.c_void_p:
         key = (tuple(src), tuple(dst), bool(centered))
@@ -154,13 +152,43 @@ def plan_covering(moduli, n: int) -> Plan:
         return p
 
 
+_CONST: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+_CONST_LOCK = threading.Lock()
+_CONST_MAX = 512
+
+
+def const_tensor(values, dtype=torch.uint64) -> torch.Tensor:
+    """A small immutable device array (Galois elements, key / diagonal pointer
+    arrays, Shoup constants), uploaded once per distinct content and reused:
+    no host-to-device copy on repeat calls.  Keyed by the values themselves,
+    so an entry can never go stale; callers must not write to it."""
+    key = (dtype, tuple(int(v) for v in values))
+    with _CONST_LOCK:
+        t = _CONST.get(key)
+        if t is not None:
+            _CONST.move_to_end(key)
+            return t
+    np_dt = {torch.uint64: np.uint64, torch.int64: np.int64, torch.int32: np.int32}[dtype]
+    t = torch.from_numpy(np.array(key[1], dtype=np_dt)).to("cuda")
+    with _CONST_LOCK:
+        _CONST[key] = t
+        while len(_CONST) > _CONST_MAX:
+            _CONST.popitem(last=False)
+    return t
+
+
+def ptr_array(tensors) -> torch.Tensor:
+    """DEVICE array of the tensors' data pointers (the C ABI's key_ptrs[] / diags[])."""
+    return const_tensor([ptr(t) for t in tensors], torch.int64)
+
+
 def shoup_pairs(vals, moduli) -> torch.Tensor:
-    """[(c, floor(c*2^64/q))] per row as a flat cuda uint64 tensor."""
+    """[(c, floor(c*2^64/q))] per row as a flat cuda uint64 tensor (cached on the device)."""
     out = []
     for c, q in zip(vals, moduli):
         c = int(c) % q
         out += [c, (c << 64) // q]
-    return torch.tensor(np.array(out, dtype=np.uint64), device="cuda")
+    return const_tensor(out)
 
 
 def fill_uniform(out: torch.Tensor, keys: np.ndarray, qs: np.ndarray, logn: int) -> None:

@@ -190,7 +190,7 @@ class Workload:
 
     name: str
     params: CkksParams
-    kind: str                       # "rotate" | "ntt" | "bsgs"
+    kind: str                       # "rotate" | "ntt" | "bsgs" | "relin"
     units: int                      # rotations / limb-batch / transforms
     desc: str = ""
     extra: dict = field(default_factory=dict, compare=False, hash=False)
@@ -217,6 +217,11 @@ def config(name: str) -> Workload:
         p = _params(16, 54, 24, 60, 8, 3)
         return Workload("C3", p, "rotate", 64,
                         "64 independent rotation key-switches, N=2^16, L=24x54b, dnum=3, K=8x60b")
+    if name == "C3M":
+        p = _params(16, 54, 24, 60, 8, 3)
+        return Workload("C3M", p, "relin", 64,
+                        "64 independent new_mult relinearisations (ModUp, KSKIP, pmodup, ModDown "
+                        "by P*q_last), one shared relin key, N=2^16, L=24x54b, dnum=3, K=8x60b")
     if name == "C4":
         p = _params(16, 54, 24, 60, 8, 3)
         return Workload("C4", p, "bsgs", 1,

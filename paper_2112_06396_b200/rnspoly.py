@@ -17,7 +17,7 @@ from . import _lib
 from ._lib import check
 from .device import plan_covering, ptr, shoup_pairs, stream_handle, to_dev
 
-OP_ADD, OP_SUB, OP_MUL, OP_NEG, OP_MULC, OP_COPY = range(6)
+OP_ADD, OP_SUB, OP_MUL, OP_NEG, OP_MULC, OP_COPY, OP_ADDC = range(7)
 
 
 def _poly_op(op: int, moduli, x: torch.Tensor, y: torch.Tensor | None = None,
@@ -120,6 +120,13 @@ class RnsPoly:
     def mul_scalars(self, scalars) -> "RnsPoly":
         cst = shoup_pairs(scalars, self.moduli)
         return RnsPoly(self.moduli, _poly_op(OP_MULC, self.moduli, self.data, cst=cst), self.rep)
+
+    def add_scalars(self, scalars) -> "RnsPoly":
+        """self + (per-row constant in every slot): pt_add of encode_const's
+        degree-0 polynomial (ckks.py:557-568) without materialising it."""
+        assert self.rep == "eval"
+        cst = shoup_pairs(scalars, self.moduli)
+        return RnsPoly(self.moduli, _poly_op(OP_ADDC, self.moduli, self.data, cst=cst), self.rep)
 
     def to_eval(self) -> "RnsPoly":
         if self.rep == "eval":

@@ -14,7 +14,7 @@ import torch
 
 from . import ckks, synth
 from ._lib import check, load
-from .device import fill_uniform, plan_for, ptr, stream_handle
+from .device import fill_uniform, plan_for, ptr, ptr_array, stream_handle
 from .params import galois_exponents
 
 
@@ -58,7 +58,7 @@ class RotationBatch:
                                    device="cuda")
         self.out_a = torch.empty_like(self.a)
         self.out_b = torch.empty_like(self.b)
-        self.ws = self.plan.workspace(L, B, "batch")
+        self.ws = self.plan.workspace(L, B)
 
     def run(self) -> None:
         ckks.rotate_batch(self.params, self.a, self.b, self.key_b, self.key_a, self.galois,
@@ -74,6 +74,57 @@ class RotationBatch:
 
     def output_bytes(self) -> int:
         return 2 * self.out_a.numel() * 8
+
+
+class RelinBatch:
+    """B independent relinearisations of new_mult (ckks.py:639-651) through one
+    batched ck_relin: per unit u the tensor-product rows (a3, b3, c3) at `limbs`
+    levels (TAG_CT_A / TAG_CT_B / TAG_CT2_A of unit u), ONE relinearisation key
+    (KeySet.relin is shared by every product, ckks.py:230)."""
+
+    def __init__(self, params, seed: int, units, limbs: int | None = None):
+        self.params = params
+        self.units = list(units)
+        B = len(self.units)
+        n = params.n_ring
+        L = params.limbs if limbs is None else limbs
+        self.limbs = L
+        full = params.full_moduli
+        dn = len(params.digit_spans(params.limbs))
+        self.plan = plan_for(params)
+        dev = dict(dtype=torch.uint64, device="cuda")
+        self.x = torch.empty((3, B, L, n), **dev)  # a3, b3, c3
+        keys, qs = [], []
+        for tag in (synth.TAG_CT_A, synth.TAG_CT_B, synth.TAG_CT2_A):
+            for u in self.units:
+                k, q = _row_keys(seed, u, tag, params.chain[:L]); keys += k; qs += q
+        fill_uniform(self.x, keys, qs, params.logn)
+        self.key_b = torch.empty((dn, len(full), n), **dev)
+        self.key_a = torch.empty((dn, len(full), n), **dev)
+        kkb, qkb, kka, qka = [], [], [], []
+        for j in range(dn):
+            k, q = _row_keys(seed, 998, synth.TAG_KEY_B, full, j); kkb += k; qkb += q
+            k, q = _row_keys(seed, 998, synth.TAG_KEY_A, full, j); kka += k; qka += q
+        fill_uniform(self.key_b, kkb, qkb, params.logn)
+        fill_uniform(self.key_a, kka, qka, params.logn)
+        self.out_a = torch.empty((B, L - 1, n), **dev)
+        self.out_b = torch.empty((B, L - 1, n), **dev)
+        nbytes = load().ck_relin_workspace_bytes(self.plan.h, L, B)
+        self.ws = torch.empty(nbytes // 8, **dev)
+
+    def run(self) -> None:
+        check(load().ck_relin(self.plan.h, ptr(self.x[0]), ptr(self.x[1]), ptr(self.x[2]),
+                              ptr(self.key_b), ptr(self.key_a), self.limbs, ptr(self.out_a),
+                              ptr(self.out_b), ptr(self.ws), len(self.units), stream_handle()),
+              "ck_relin")
+
+    def algorithmic_bytes_per_unit(self) -> int:
+        """Read a3, b3, c3, write two (l-1)-limb outputs; the shared key's
+        2 beta (l+K) rows once per batch."""
+        p, l = self.params, self.limbs
+        beta = len(p.digit_spans(l))
+        key = 2 * beta * (l + len(p.special))
+        return 8 * p.n_ring * (3 * l + 2 * (l - 1)) + 8 * p.n_ring * key // len(self.units)
 
 
 class NttBatch:
@@ -145,12 +196,16 @@ class BsgsWorkload:
                 qq += q
         fill_uniform(self.diags, kk, qq, params.logn)
         self.out = (torch.empty((L - 1, n), **dev), torch.empty((L - 1, n), **dev))
+        # the C ABI takes per-key / per-diagonal pointer arrays (built once)
+        self.ptrs = (ptr_array(list(self.bkb)), ptr_array(list(self.bka)),
+                     ptr_array(list(self.gkb)), ptr_array(list(self.gka)),
+                     ptr_array([self.diags[j, k] for j in range(giant) for k in range(baby)]))
         nbytes = load().ck_bsgs_workspace_bytes(self.plan.h, L, baby, giant)
         self.ws = torch.empty(nbytes // 8, **dev)
 
     def run(self) -> None:
-        ckks.bsgs_raw(self.params, self.a, self.b, self.bkb, self.bka, self.gkb, self.gka,
-                      self.diags, self.baby, self.giant, out=self.out, ws=self.ws)
+        ckks.bsgs_raw(self.params, self.a, self.b, *self.ptrs, self.baby, self.giant,
+                      out=self.out, ws=self.ws)
 
     def algorithmic_bytes(self) -> int:
         """a, b; baby keys; diagonals; giant keys (at l-1); output."""

@@ -71,6 +71,10 @@ def _toy_cases():
         ]
     out.append(Case("B_bsgs", TOY_B, "bsgs", (4, 2), True))
     out.append(Case("D_bsgs", TOY_D, "bsgs", (3, 3), True))
+    # more than 32 diagonals / baby steps (chunked accumulation): a radix-32
+    # CoeffToSlot stage has 2*32-1 = 63 diagonals (bootstrap.py:128-133)
+    out.append(Case("B_matvec63", TOY_B, "pt_matvec", (tuple(range(-31, 32)),), True))
+    out.append(Case("D_bsgs40", TOY_D, "bsgs", (40, 2), True))
     return out
 
 
@@ -81,10 +85,15 @@ def full_cases():
         Case("C1_rot", ("cfg", "C1"), "rotate_k", (0, 1)),
         Case("C2_ntt", ("cfg", "C2"), "ntt", ()),
         Case("C2_intt", ("cfg", "C2"), "intt", ()),
+        # the whole C2 batch (16 polynomials x 24 limbs) forward and inverse
+        Case("C2_ntt_b16", ("cfg", "C2"), "ntt_batch", (16, False)),
+        Case("C2_intt_b16", ("cfg", "C2"), "ntt_batch", (16, True)),
         Case("C3_rot0", ("cfg", "C3"), "rotate_k", (0, c3k[0])),
         Case("C3_rot1", ("cfg", "C3"), "rotate_k", (1, c3k[1])),
         Case("C3_rot63", ("cfg", "C3"), "rotate_k", (63, c3k[63])),
         Case("C3_conj", ("cfg", "C3"), "conjugate", (None,)),
+        # hoisted: the 16 baby rotations of C4 (k = 1..16) from one shared ModUp
+        Case("C3_hrot16", ("cfg", "C3"), "hrotate", (tuple(-k for k in range(1, 17)), None)),
         Case("C3_new_mult", ("cfg", "C3"), "new_mult", (1, None)),
         Case("C4_bsgs", ("cfg", "C4"), "bsgs", (16, 8)),
         Case("C5_rot0", ("cfg", "C5"), "rotate_k", (0, c5k[0])),
@@ -141,6 +150,13 @@ def run_case(case: Case, be):
         mods = full if case.pspec[0] == "toy" else p.chain
         x = _rows(p, 0, synth.TAG_NTT, mods)
         return (be.ntt(x, mods) if op == "ntt" else be.intt(x, mods),)
+    if op == "ntt_batch":
+        units, inverse = case.args
+        xs = np.stack([_rows(p, u, synth.TAG_NTT, p.chain) for u in range(units)])
+        if hasattr(be, "ntt_batch"):
+            return tuple(be.ntt_batch(xs, p.chain, inverse))
+        f = be.intt if inverse else be.ntt
+        return tuple(f(x, p.chain) for x in xs)
     if op == "bc_convert":
         src, dst = p.chain[:p.alpha], p.chain[p.alpha:] + p.special
         return (be.bc_convert(_rows(p, 0, synth.TAG_NTT, src), src, dst),)

@@ -29,6 +29,18 @@ class GpuBackend:
     def intt(self, x, mods):
         return to_host(rnspoly.ntt_rows(to_dev(x), tuple(mods), True))
 
+    def ntt_batch(self, xs, mods, inverse):
+        """The whole [batch][limbs][N] array in ONE ck_ntt call (batch indexing)."""
+        from paper_2112_06396_b200._lib import check, load
+        from paper_2112_06396_b200.device import plan_covering, ptr, stream_handle
+        x = to_dev(xs)
+        B, L, n = x.shape
+        plan = plan_covering(tuple(mods), n)
+        idx = plan.prime_idx(tuple(mods))
+        check(load().ck_ntt(plan.h, ptr(x), ptr(idx), L, B, L * n, int(inverse), stream_handle()),
+              "ck_ntt")
+        return list(to_host(x))
+
     def bc_convert(self, x, src, dst):
         return to_host(rnspoly.bc_convert(RnsPoly(src, x, "coeff"), dst).data)
 

@@ -125,10 +125,13 @@ def test_relin_argument_errors():
     p = _params(12, 4, 1, 4)
     lib = _lib.load()
     h = plan_for(p).h
-    assert lib.ck_relin_workspace_bytes(h, 1) == 0          # merged ModDown needs l >= 2
-    assert lib.ck_relin_workspace_bytes(h, p.limbs) > 0
+    assert lib.ck_relin_workspace_bytes(h, 1, 1) == 0          # merged ModDown needs l >= 2
+    assert lib.ck_relin_workspace_bytes(h, p.limbs, 0) == 0    # empty batch
+    assert lib.ck_relin_workspace_bytes(h, p.limbs, 1) > 0
     x = torch.zeros((p.limbs, p.n_ring), dtype=torch.uint64, device="cuda")
     assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), None, None, p.limbs,
-                        x.data_ptr(), x.data_ptr(), x.data_ptr(), None) == _lib.CK_ERR_ARG
+                        x.data_ptr(), x.data_ptr(), x.data_ptr(), 1, None) == _lib.CK_ERR_ARG
     assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), 1,
-                        x.data_ptr(), x.data_ptr(), x.data_ptr(), None) == _lib.CK_ERR_ARG
+                        x.data_ptr(), x.data_ptr(), x.data_ptr(), 1, None) == _lib.CK_ERR_ARG
+    assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(),
+                        p.limbs, x.data_ptr(), x.data_ptr(), x.data_ptr(), 0, None) == _lib.CK_ERR_ARG

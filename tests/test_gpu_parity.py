@@ -43,8 +43,9 @@ def test_toy_case_fused_rotate_entry(case):
     _check_toy(case, cases.run_case(case, GpuRotateBackend()))
 
 
-@pytest.mark.parametrize("name", ["C1_rot", "C2_ntt", "C2_intt", "C3_rot0", "C3_rot1", "C3_rot63",
-                                  "C3_conj", "C3_new_mult", "C5_rot0", "C5_rot255"])
+@pytest.mark.parametrize("name", ["C1_rot", "C2_ntt", "C2_intt", "C2_ntt_b16", "C2_intt_b16",
+                                  "C3_rot0", "C3_rot1", "C3_rot63", "C3_conj", "C3_hrot16",
+                                  "C3_new_mult", "C5_rot0", "C5_rot255"])
 def test_full_config_digest(name):
     out = cases.run_case(FULL[name], GpuRotateBackend())
     assert digest(*out) == GOLD[name]["digest"], name
