@@ -54,22 +54,6 @@ def ks_bytes(params, limbs=None) -> int:
     return 8 * params.n_ring * (l + l + 2 * beta * (l + K) + 2 * l)
 
 
-def int_slots_per_ks(params, limbs=None) -> float:
-    """Analytic IMAD-pipe slots of one rotation key-switch:
-    160 limb NTTs x N/2 log N Shoup butterflies (18 slots), base conversions
-    (8 slots per source MAC + 26 per reduction), KSKIP (6 MACs + 2 reductions)."""
-    l = params.limbs if limbs is None else limbs
-    K = len(params.special)
-    spans = params.digit_spans(l)
-    beta, R, n, logn = len(spans), l + K, params.n_ring, params.logn
-    ntt_limbs = l + sum(R - (hi - lo) for lo, hi in spans) + 2 * K + 2 * l
-    bfly = ntt_limbs * (n // 2) * logn * 18
-    bc = sum((R - (hi - lo)) * ((hi - lo) * 8 + 26) for lo, hi in spans) * n
-    bc += 2 * l * (K * 8 + 26) * n
-    ks = R * n * (2 * beta * 8 + 2 * 28)
-    return float(bfly + bc + ks)
-
-
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -130,26 +114,133 @@ def _cpu_task(args):
     return unit, time.perf_counter() - t0, digest(oa, ob)
 
 
-def _warm(_):
+def _warm(name="C3"):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import ckks_np
     from paper_2112_06396_b200.params import config
-    p = config("C3").params
+    p = config(name).params
     for q in p.full_moduli:
         ckks_np.twiddles(q, p.n_ring)
     return True
+
+
+# ---- per-config CPU baseline units (the oracle port of the reference, one unit per
+# task; bench.py's cpu_baseline leg is the only product-side caller of oracle/)
+def _cpu_unit(args):
+    """(config, unit, extra) -> (unit, seconds, digest of the unit's outputs)."""
+    name, unit, extra = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import ckks_np
+    from paper_2112_06396_b200 import synth
+    from paper_2112_06396_b200.digest import digest
+    from paper_2112_06396_b200.params import config
+    p = config(name).params
+    if name in ("C1", "C3", "C5"):
+        a, b, kb, ka = synth.rotation_inputs(p, SEED, unit)
+        t0 = time.perf_counter()
+        out = ckks_np.rotate_galois(p, a, b, kb, ka, pow(5, extra, 2 * p.n_ring))
+    elif name == "C2":  # one polynomial (all limbs) forward, then its inverse
+        x = synth.uniform_poly(SEED, unit, synth.TAG_NTT, p.chain, p.n_ring)
+        t0 = time.perf_counter()
+        f = ckks_np.ntt(x, p.chain)
+        inv = ckks_np.intt(x, p.chain)
+        out = (f,)
+        assert inv.shape == x.shape
+    elif name == "C3M":  # relinearisation of unit `unit`, shared relin key (unit 998)
+        mods = p.chain
+        a3, b3, c3 = (synth.uniform_poly(SEED, unit, tag, mods, p.n_ring)
+                      for tag in (synth.TAG_CT_A, synth.TAG_CT_B, synth.TAG_CT2_A))
+        kb, ka = synth.switching_key(p, SEED, 998)
+        t0 = time.perf_counter()
+        lim = len(mods)
+        digits = ckks_np.decomp_modup(p, a3, mods)
+        u, v = ckks_np.kskip(p, digits, kb, ka, lim)
+        qr = ckks_np._qcol(p.raised_moduli(lim), 2)
+        u = ckks_np.addmod(u, ckks_np.pmodup(p, b3, mods), qr)
+        v = ckks_np.addmod(v, ckks_np.pmodup(p, c3, mods), qr)
+        out = (ckks_np.moddown_merged(p, u, lim), ckks_np.moddown_merged(p, v, lim))
+    else:
+        raise KeyError(name)
+    return unit, time.perf_counter() - t0, digest(*out)
+
+
+def _c4_stage(args):
+    """One stage of the hoisted C4 BSGS transform on the CPU (oracle port), with
+    intermediates in a RAM-backed directory (numpy files, memory-mapped by the
+    next stage's workers instead of pickled through pipes):
+    ('modup', dir) -> digits; ('baby', dir, k) -> (u_k, v_k + P b_k);
+    ('giant', dir, j) -> rotate(ModDown(sum_k diag[j][k] (u_k, v_k)), -16 j)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+    from oracle import ckks_np
+    from paper_2112_06396_b200 import synth
+    from paper_2112_06396_b200.params import config
+    p = config("C4").params
+    n, L = p.n_ring, p.limbs
+    mods, raised = p.chain, p.raised_moduli(L)
+    qr = ckks_np._qcol(raised, 2)
+    kind, d = args[0], args[1]
+    if kind == "modup":
+        a = synth.uniform_poly(SEED, 0, synth.TAG_CT_A, mods, n)
+        np.save(os.path.join(d, "digits.npy"), np.stack(ckks_np.decomp_modup(p, a, mods)))
+        return True
+    if kind == "baby":
+        k = args[2]
+        digits = np.load(os.path.join(d, "digits.npy"), mmap_mode="r")
+        b = synth.uniform_poly(SEED, 0, synth.TAG_CT_B, mods, n)
+        kb, ka = synth.switching_key(p, SEED, 1000 + ((-k) % (4 * n)))
+        perm = ckks_np.automorph_perm(n, ckks_np.galois_rot(n, -k))
+        u, v = ckks_np.kskip(p, [np.asarray(x)[:, perm] for x in digits], kb, ka, L)
+        v = ckks_np.addmod(v, ckks_np.pmodup(p, b[:, perm], mods), qr)
+        np.save(os.path.join(d, f"baby{k}.npy"), np.stack([u, v]))
+        return True
+    j = args[2]
+    acc_u = np.zeros((len(raised), n), dtype=np.uint64)
+    acc_v = np.zeros_like(acc_u)
+    for k in range(1, 17):
+        uv = np.load(os.path.join(d, f"baby{k}.npy"), mmap_mode="r")
+        m = synth.uniform_poly(SEED, j, synth.TAG_DIAG, raised, n, digit=k)
+        acc_u = ckks_np.addmod(acc_u, ckks_np.mulmod(m, np.asarray(uv[0]), qr), qr)
+        acc_v = ckks_np.addmod(acc_v, ckks_np.mulmod(m, np.asarray(uv[1]), qr), qr)
+    ga, gb = ckks_np.moddown_merged(p, acc_u, L), ckks_np.moddown_merged(p, acc_v, L)
+    r = -16 * j
+    kb, ka = synth.switching_key(p, SEED, 1000 + (r % (4 * n)))
+    return ckks_np.rotate_galois(p, ga, gb, kb, ka, ckks_np.galois_rot(n, r))
+
+
+def cpu_c4_transform(pool):
+    """One C4 transform, hoisted, stages parallel across the pool (ModUp; 16 babies;
+    8 giant groups each MAC + ModDown + rotation; sum).  Returns (seconds, digest)."""
+    import shutil
+    from oracle import ckks_np
+    from paper_2112_06396_b200.digest import digest
+    from paper_2112_06396_b200.params import config
+    p = config("C4").params
+    d = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    try:
+        t0 = time.perf_counter()
+        pool.apply(_c4_stage, (("modup", d),))
+        pool.map(_c4_stage, [("baby", d, k) for k in range(1, 17)], chunksize=1)
+        giants = pool.map(_c4_stage, [("giant", d, j) for j in range(1, 9)], chunksize=1)
+        ql = ckks_np._qcol(p.chain[:p.limbs - 1], 2)
+        oa, ob = giants[0]
+        for ga, gb in giants[1:]:
+            oa, ob = ckks_np.addmod(oa, ga, ql), ckks_np.addmod(ob, gb, ql)
+        return time.perf_counter() - t0, digest(oa, ob)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
 
 
 def _init_worker():
     os.environ["OMP_NUM_THREADS"] = "1"
 
 
-def cpu_pool(wait: bool = True):
+def cpu_pool(wait: bool = True, name: str = "C3"):
     """Fork the CPU workers BEFORE CUDA is initialised in this process."""
     workers = max(1, min(os.cpu_count() or 1, CPU_WORKERS_MAX))
     ctx = mp.get_context("fork")
     pool = ctx.Pool(workers, initializer=_init_worker)
-    warm = pool.map_async(_warm, range(workers))
+    warm = pool.map_async(_warm, [name] * workers)
     if wait:
         warm.wait()
     return pool, workers
@@ -261,30 +352,27 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peak, peak_kind = _peaks()
     bytes_ks = ks_bytes(p)
     achieved = bytes_ks * B / (ms_step / 1000.0) / 1e9
-    traffic = args.traffic
-    if traffic is None:
-        try:  # committed ncu measurement (profiles/r01_traffic.json), per launch = per unit x B
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))[
-                "c3_dram_bytes_per_keyswitch"] * B
-        except Exception:
-            traffic = None
+    traffic, tr_src = args.traffic, "--traffic"
+    tr_all = {}
+    try:
+        tr_all = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json"))).get("C3", {})
+    except Exception:
+        pass
+    if traffic is None and tr_all:
+        traffic, tr_src = tr_all["dram_bytes_per_unit"] * B, "profiles/r02_traffic.json: " + tr_all["source"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "traffic_source": "profiles/r01_traffic.json (ncu dram bytes of one step, all launches)",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": tr_src,
                 "kernel": "ck_rotate pipeline (batched key-switch, all launches of one step)",
                 "algorithmic_bytes_per_unit": bytes_ks, "units_per_launch": B,
                 "peak_kind": peak_kind}
-    # The path is INT-issue bound: report the IMAD-pipe
-    # roofline too.  Slots = analytic IMAD-pipe slots per key-switch; peak =
-    # 64 IMAD slots/clk/SM (profiles/r01_microbench_int.txt) x SMs x clock.
-    props = torch.cuda.get_device_properties(local_rank)
-    clk_mhz = clocks.get("sm_mhz") or 1965.0
-    slots = int_slots_per_ks(p)
-    int_peak = props.multi_processor_count * 64 * clk_mhz * 1e6
-    int_ach = slots * B / (ms_step / 1000.0)
-    roofline["int_pipe"] = {"bound": "imad", "achieved_slots_per_s": int_ach, "peak_slots_per_s": int_peak,
-                            "frac": int_ach / int_peak, "slots_per_unit": slots,
-                            "note": "18 IMAD slots per Shoup butterfly, 8 per 30-bit-split MAC, ~28 per reduction"}
+    # The path is bound by the fma-heavy (IMAD) pipe, not by HBM:
+    # its MEASURED utilisation, time-weighted over the step's kernels (ncu
+    # sm__pipe_fmaheavy_cycles_active, committed with the launch list).
+    if tr_all.get("fmaheavy_time_weighted_pct") is not None:
+        roofline["int_pipe"] = {"bound": "fma-heavy pipe (IMAD)",
+                                "frac": tr_all["fmaheavy_time_weighted_pct"] / 100.0,
+                                "source": "ncu sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_"
+                                          "elapsed per kernel, weighted by kernel time (profiles/r02_traffic.json)"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -421,11 +509,27 @@ def e2e_compressed(args, p, B, world, wb, host_in, host_out, pipe, stream, max_o
                                          torch.equal(ob.cpu(), host_out[1][:m]))
     return out
 
+def _traffic(name: str):
+    """ncu DRAM bytes per unit of a config from the committed launch-list summary
+    (profiles/r02_traffic.json, written by tools/traffic_json.py), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+        return d[name]["dram_bytes_per_unit"], d[name]["source"]
+    except Exception:
+        return None, None
+
+
 def run_config(args, rank: int, world: int, local_rank: int):
-    """Non-default BASELINE configs (C1, C2, C4, C5): device-resident throughput only."""
+    """BASELINE configs C1, C2, C4, C5 and the relinearisation workload C3M: device-
+    resident throughput, roofline, clocks and the CPU baseline (oracle port of the
+    reference on the host cores, rank 0 at N=1) in one line."""
+    pool = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        pool, workers = cpu_pool(wait=False, name=args.config)
     import torch
     import torch.distributed as dist
     from paper_2112_06396_b200 import _lib
+    from paper_2112_06396_b200.digest import digest
     from paper_2112_06396_b200.params import config, galois_exponents
     from paper_2112_06396_b200 import workload as W
 
@@ -435,21 +539,27 @@ def run_config(args, rank: int, world: int, local_rank: int):
     lib = _lib.load()
     wl = config(args.config)
     p = wl.params
+    ks = None
     if wl.kind == "rotate":
         B = args.batch if args.batch_set else {"C1": 1, "C5": 32}.get(args.config, 64)
         units = [rank * B + i for i in range(B)]
         allk = galois_exponents(p.n_ring, B * world, SEED)
-        job = W.RotationBatch(p, SEED, units, ks=[allk[u] for u in units])
+        # C1 is "HRotate by k=1 (Galois element 5)" (BASELINE.json configs[0])
+        ks = [1] * B if args.config == "C1" else [allk[u] for u in units]
+        job = W.RotationBatch(p, SEED, units, ks=ks)
         per_step, unit, bytes_unit = B, "key-switches/s", ks_bytes(p)
     elif wl.kind == "relin":
         B = args.batch
-        job = W.RelinBatch(p, SEED, [rank * B + i for i in range(B)])
+        units = [rank * B + i for i in range(B)]
+        job = W.RelinBatch(p, SEED, units)
         per_step, unit, bytes_unit = B, "relinearisations/s", job.algorithmic_bytes_per_unit()
     elif wl.kind == "ntt":
+        units = list(range(16))
         job = W.NttBatch(p, SEED, 16)
         per_step, unit = 16 * p.limbs, "limb NTT+INTT round trips/s"
         bytes_unit = 4 * 8 * p.n_ring
     else:
+        units = [0]
         job = W.BsgsWorkload(p, SEED)
         per_step, unit, bytes_unit = 1, "BSGS transforms/s", job.algorithmic_bytes()
     for _ in range(args.warmup):
@@ -480,21 +590,41 @@ def run_config(args, rank: int, world: int, local_rank: int):
         for _ in range(args.warmup):
             graph.replay()
         torch.cuda.synchronize()
+    # inputs smaller than L2 (C1: 1.8 MB per step) -> flush L2 between timed steps
+    # (a 256 MB write outside the per-step event pairs)
+    in_bytes = getattr(job, "input_bytes", lambda: 1 << 40)()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if in_bytes < (256 << 20) else None
     if world > 1:
         dist.barrier()
-    n0 = lib.ck_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
-            job.run()
-    e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    clk = ClockSampler(local_rank)
+    clk.start()
+    n0 = lib.ck_launch_count()
+    step = (lambda: graph.replay()) if graph is not None else job.run
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for e0, e1 in evs:
+            flush.add_(1)
+            e0.record()
+            step()
+            e1.record()
+        torch.cuda.synchronize()
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     launches = (launches_per_step * args.steps if graph is not None
                 else lib.ck_launch_count() - n0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -502,12 +632,45 @@ def run_config(args, rank: int, world: int, local_rank: int):
     peak, peak_kind = _peaks()
     ms_step = ms / args.steps
     achieved = bytes_unit * per_step / (ms_step / 1000.0) / 1e9
+    tr_unit, tr_src = _traffic(args.config)
     extra = {}
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
     if wl.kind == "bsgs" and rank == 0:
-        from paper_2112_06396_b200.digest import digest
-        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
         extra["parity_vs_reference_digest"] = (
             digest(job.out[0].cpu().numpy(), job.out[1].cpu().numpy()) == gold["C4_bsgs"]["digest"])
+
+    # ---- CPU baseline: the oracle port of the reference on the host cores (bounded sample)
+    cpu = None
+    if pool is not None:
+        if wl.kind == "bsgs":
+            wall, dg = cpu_c4_transform(pool)
+            cpu = {"value": 1.0 / wall, "unit": unit, "cores": workers, "kind": "port",
+                   "sample": "one C4 transform, hoisted (ModUp; 16 baby KSKIPs in parallel; 8 giant "
+                             "groups (MAC + merged ModDown + rotation) in parallel; sum), numpy port",
+                   "parity_vs_gpu_bit_exact": dg == gold["C4_bsgs"]["digest"]}
+        else:
+            n_s = {"C1": 8 * workers, "C2": workers}.get(args.config, workers)
+            if wl.kind == "rotate":
+                tasks = [(args.config, units[i % len(units)], ks[i % len(units)]) for i in range(n_s)]
+            else:
+                tasks = [(args.config, units[i % len(units)], None) for i in range(n_s)]
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_unit, tasks, chunksize=1)
+            wall = time.perf_counter() - t0
+            per_task = p.limbs if wl.kind == "ntt" else 1
+            if wl.kind == "ntt":
+                parity = res[0][2] == gold["C2_ntt"]["digest"]
+                what = "polynomials of 24 limbs (forward NTT then inverse, one per task)"
+            else:
+                outs = {u: digest(job.out_a[i].cpu().numpy(), job.out_b[i].cpu().numpy())
+                        for i, u in enumerate(units)}
+                parity = all(dg == outs[u] for u, _, dg in res)
+                what = {"rotate": "rotation key-switches", "relin": "relinearisations"}[wl.kind]
+            cpu = {"value": n_s * per_task / wall, "unit": unit, "cores": workers, "kind": "port",
+                   "sample": f"{n_s} {what} of this workload, one per task on {workers} worker "
+                             "processes (numpy port of the reference, oracle/ckks_np.py)",
+                   "parity_vs_gpu_bit_exact": parity}
+        pool.close()
     if rank == 0:
         print(json.dumps({
             "metric": f"{unit} ({args.config})", "value": per_step * world * args.steps / (ms / 1000.0),
@@ -515,11 +678,15 @@ def run_config(args, rank: int, world: int, local_rank: int):
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, generated on device)",
             "config": {"workload": wl.desc, "units_per_gpu_per_step": per_step,
-                       "cuda_graph": graph is not None},
+                       "global_units_per_step": per_step * world, "cuda_graph": graph is not None,
+                       "l2": ("flushed between timed steps (256 MB write outside the events)"
+                              if flush is not None else "inputs larger than L2, no flush")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "algorithmic_bytes_per_unit": bytes_unit, "peak_kind": peak_kind},
-            "gpu_launches": launches, **extra}), flush=True)
+                         "frac": achieved / peak,
+                         "traffic": tr_unit * per_step if tr_unit else None, "traffic_source": tr_src,
+                         "algorithmic_bytes_per_unit": bytes_unit, "units_per_launch": per_step,
+                         "peak_kind": peak_kind},
+            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks, **extra}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

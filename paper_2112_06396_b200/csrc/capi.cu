@@ -158,6 +158,7 @@ struct LevelTab {
 struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
+  bool kc = false;    // chain-row KSKIP+ModDown kernel (CKB200_KC=1; measured slower, see DESIGN)
   int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
@@ -688,7 +689,11 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
   ka_.R = (int)R;
   ka_.logn = p->logn;
   ka_.key_prefetch = p->key_prefetch;
-  CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
+  // chain-row kernel: ks_row only produces the rows ModDown drops (specials, and
+  // q_last for relinearisation); the kept rows' KSKIP runs inside kc_row below
+  const bool kc = p->kc && t.beta <= 4;
+  ka_.row0 = kc ? (int)keep : 0;
+  CK_TRY(ck::launch_ks_row(ka_, (int)(R - ka_.row0), B, st));
   if (relin) {
     // pmodup (ckks.py:478-489) on the dropped chain row q_last: it feeds the BC
     const int* lp = t.d_chain_prime + (l - 1);
@@ -708,6 +713,47 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
     CK_TRY(ck::launch_bconv(g1, 2 * B, st));
     CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, keep * N, false,
                      1, st));
+  }
+  if (kc) {
+    // ---- kept chain rows: KSKIP + fwd row phase of the converted rows + epilogue, one launch
+    ck::KcRowArgs kr{};
+    kr.a_eval = a_src;
+    kr.a_batch = l * N;
+    kr.dig = w.dig;
+    kr.dig_batch = dig_b;
+    kr.key_b = keys.b;
+    kr.key_a = keys.a;
+    kr.key_b_ptrs = keys.bp;
+    kr.key_a_ptrs = keys.ap;
+    kr.key_digit_stride = ka_.key_digit_stride;
+    kr.key_batch = ka_.key_batch;
+    kr.prime = t.d_raised_prime;  // kept rows j < keep: raised row j == chain row j
+    kr.pc = p->d_pc;
+    kr.tw = p->d_tw;
+    kr.galois = kgal;
+    kr.galois_t = kgt;
+    for (int d = 0; d < 16; ++d) {
+      kr.lo[d] = ka_.lo[d];
+      kr.hi[d] = ka_.hi[d];
+    }
+    kr.beta = t.beta;
+    kr.R = (int)R;
+    kr.logn = p->logn;
+    kr.key_prefetch = p->key_prefetch;
+    kr.conv = w.conv;
+    kr.conv_batch = 2 * keep * N;
+    kr.conv_w = keep * N;
+    kr.pinv = m.d_pinv;
+    kr.add_u = relin ? relin->b3 : nullptr;
+    kr.add_v = relin ? relin->c3 : b_add;
+    kr.add_batch = l * N;
+    kr.add_scale = relin ? m.d_dinv : nullptr;
+    kr.egalois = relin ? nullptr : egal;
+    kr.egalois_t = relin ? 1 : egt;
+    kr.out_a = out_a;
+    kr.out_b = out_b;
+    kr.out_batch = keep * N;
+    return ck::launch_kc_row(kr, (int)keep, B, st);
   }
   // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
   ck::MdRowArgs ma{};
@@ -775,6 +821,8 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   {
     const char* e = getenv("CKB200_UNFUSED");
     p->fused = !(e && e[0] == '1');
+    const char* kc = getenv("CKB200_KC");
+    p->kc = kc && kc[0] == '1';
     const char* tc = getenv("CKB200_BCTC");
     if (tc) p->bc_tc = atoi(tc);
   }

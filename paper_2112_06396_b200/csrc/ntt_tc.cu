@@ -107,15 +107,84 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // quotient qh = round(vhi 2^32 / p) from vhi = floor(V / 2^32) (exact in a
 // double); the dropped low part adds < 2^48 / p < 0.36 to the error, so
 // |V/p - qh| < 1 and V - qh p + p lands in (0, 2p), computed mod 2^64.
+// Written in PTX so the byte-plane assembly stays on the ALU pipe (shifts,
+// add.cc/addc) instead of ptxas's IMAD / IMAD.WIDE-by-2^16 forms: the
+// fma-heavy pipe only sees the qh * p product (one mul.wide + one mad).
 __device__ __forceinline__ u64 reduce_lazy(const uint32_t* s, u64 p, double pinv32) {
   const u32 P0 = s[0] + (s[1] << 8), P1 = s[2] + (s[3] << 8);
   const u32 P2 = s[4] + (s[5] << 8), P3 = s[6] + (s[7] << 8);
-  const u64 vlo = (u64)P0 + ((u64)P1 << 16) + ((u64)P2 << 32) + ((u64)P3 << 48);
-  const u64 vhi = ((u64)P3 << 16) + P2;  // < 2^49
-  const double vd = __dsub_rn(__longlong_as_double((long long)(vhi | 0x4330000000000000ull)),
-                              4503599627370496.0);
+  u32 lo, hi, ml, mh;
+  // vlo = P0 + P1 2^16 + P2 2^32 + P3 2^48 (mod 2^64)
+  asm("{\n\t.reg .u32 t0, t1;\n\t"
+      "shl.b32 t0, %2, 16;\n\t"
+      "shr.u32 t1, %2, 16;\n\t"
+      "add.cc.u32 %0, %3, t0;\n\t"
+      "shl.b32 t0, %5, 16;\n\t"
+      "addc.u32 %1, %4, t0;\n\t"
+      "add.u32 %1, %1, t1;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(P1), "r"(P0), "r"(P2), "r"(P3));
+  // vhi = P3 2^16 + P2 < 2^49, as a double via the 2^52 magic (exact)
+  asm("{\n\t.reg .u32 t0;\n\t"
+      "shl.b32 t0, %2, 16;\n\t"
+      "add.cc.u32 %0, %3, t0;\n\t"
+      "shr.u32 t0, %2, 16;\n\t"
+      "addc.u32 %1, t0, 0x43300000;\n\t}"
+      : "=r"(ml), "=r"(mh)
+      : "r"(P3), "r"(P2));
+  const double vd = __dsub_rn(__hiloint2double((int)mh, (int)ml), 4503599627370496.0);
   const u32 qh = (u32)__double2loint(__fma_rn(vd, pinv32, 6755399441055744.0));
-  return vlo - (u64)qh * p + p;
+  // r = vlo + p - qh p  (mod 2^64)
+  const u32 pl = (u32)p, ph = (u32)(p >> 32);
+  u32 rl, rh;
+  asm("{\n\t.reg .u32 m0, m1;\n\t"
+      "mul.lo.u32 m0, %4, %2;\n\t"
+      "mul.hi.u32 m1, %4, %2;\n\t"
+      "mad.lo.u32 m1, %4, %3, m1;\n\t"
+      "add.cc.u32 %0, %5, %2;\n\t"
+      "addc.u32 %1, %6, %3;\n\t"
+      "sub.cc.u32 %0, %0, m0;\n\t"
+      "subc.u32 %1, %1, m1;\n\t}"
+      : "=r"(rl), "=r"(rh)
+      : "r"(pl), "r"(ph), "r"(qh), "r"(lo), "r"(hi));
+  return ((u64)rh << 32) | rl;
+}
+
+// x * w mod p into [0, 4p) for x < 2^56, w < p, wp = floor(w 2^64 / p): Shoup
+// with a 3-product quotient q1 = xh wph + hi(xh wpl) + hi(xl wph) (xh = x >> 32)
+// that undershoots floor(x wp / 2^64) by at most 2 (two dropped fractional
+// carries + the dropped xl wpl term), so the remainder grows by at most 2p.
+// The next tensor-core pass accepts any 64-bit operand; canonical outputs
+// fold it with two conditional subtractions.
+__device__ __forceinline__ u64 shoup_tc(u64 x, u64 w, u64 wp, u64 p) {
+  const u32 xl = (u32)x, xh = (u32)(x >> 32);
+  const u32 wl = (u32)w, wh = (u32)(w >> 32);
+  const u32 wpl = (u32)wp, wph = (u32)(wp >> 32);
+  const u32 pl = (u32)p, ph = (u32)(p >> 32);
+  u32 rl, rh;
+  asm("{\n\t.reg .u32 q0, q1, a, b, c0, c1;\n\t"
+      // q1 = xh * wph + hi(xh * wpl) + hi(xl * wph)  (64-bit)
+      "mul.hi.u32 a, %3, %7;\n\t"
+      "mul.hi.u32 b, %2, %8;\n\t"
+      "mad.lo.cc.u32 q0, %3, %8, a;\n\t"
+      "madc.hi.u32 q1, %3, %8, 0;\n\t"
+      "add.cc.u32 q0, q0, b;\n\t"
+      "addc.u32 q1, q1, 0;\n\t"
+      // x * w (mod 2^64)
+      "mul.lo.u32 c0, %2, %4;\n\t"
+      "mul.hi.u32 c1, %2, %4;\n\t"
+      "mad.lo.u32 c1, %2, %5, c1;\n\t"
+      "mad.lo.u32 c1, %3, %4, c1;\n\t"
+      // - q1 * p (mod 2^64)
+      "mul.lo.u32 a, q0, %9;\n\t"
+      "mul.hi.u32 b, q0, %9;\n\t"
+      "mad.lo.u32 b, q0, %10, b;\n\t"
+      "mad.lo.u32 b, q1, %9, b;\n\t"
+      "sub.cc.u32 %0, c0, a;\n\t"
+      "subc.u32 %1, c1, b;\n\t}"
+      : "=r"(rl), "=r"(rh)
+      : "r"(xl), "r"(xh), "r"(wl), "r"(wh), "r"(0), "r"(wpl), "r"(wph), "r"(pl), "r"(ph));
+  return ((u64)rh << 32) | rl;
 }
 
 __device__ __forceinline__ void st_u64(unsigned char* base, int row, int elem, u64 v) {
@@ -233,7 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
           const int o = h * 4 + u;                      // pass-1 output index
           const u64 y = reduce_lazy(sv + 8 * u, p, pinv32);
           const ulonglong2 d = tw[o * 16 + g1];
-          st_u64(A, o * 8 + c, g1, shoup_lazy(y, d.x, d.y, p));  // [0, 2p)
+          st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, p));  // [0, 4p)
         }
       }
     }
@@ -265,7 +334,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
           const int o2 = h * 4 + u;
           const u64 v = reduce_lazy(sv + 8 * u, p, pinv32);
           if (INV)  // rows 16 o2 + o1; canonical (the base conversion needs exact residues)
-            col[(long long)(o2 * 16 + o1) << P2] = shoup(v, scl.x, scl.y, p);
+            col[(long long)(o2 * 16 + o1) << P2] = csub(csub(shoup_tc(v, scl.x, scl.y, p), 2 * p), p);
           else      // rows 16 o1 + o2; lazy (0, 2p)
             col[(long long)(o1 * 16 + o2) << P2] = v;
         }

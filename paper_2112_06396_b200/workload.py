@@ -119,12 +119,16 @@ class RelinBatch:
               "ck_relin")
 
     def algorithmic_bytes_per_unit(self) -> int:
-        """Read a3, b3, c3, write two (l-1)-limb outputs; the shared key's
-        2 beta (l+K) rows once per batch."""
-        p, l = self.params, self.limbs
-        beta = len(p.digit_spans(l))
-        key = 2 * beta * (l + len(p.special))
-        return 8 * p.n_ring * (3 * l + 2 * (l - 1)) + 8 * p.n_ring * key // len(self.units)
+        return relin_bytes(self.params, self.limbs, len(self.units))
+
+
+def relin_bytes(p, l: int, batch: int) -> int:
+    """Compulsory HBM bytes per relinearisation in a batch sharing one key: read
+    a3, b3, c3 (3 l limbs), write two (l-1)-limb outputs, and the key's
+    2 beta (l+K) rows once per batch."""
+    beta = len(p.digit_spans(l))
+    key = 2 * beta * (l + len(p.special))
+    return 8 * p.n_ring * (3 * l + 2 * (l - 1)) + 8 * p.n_ring * key // batch
 
 
 class NttBatch:
