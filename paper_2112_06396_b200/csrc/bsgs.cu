@@ -23,73 +23,117 @@ constexpr int kMaxBaby = 32;
 // inputs stay in registers; entries k >= baby are never touched).  A thread
 // owns one coefficient of one raised row for BOTH u and v, so every diagonal
 // element is loaded once and feeds two accumulators.
+constexpr int kDiagKL = 8;      // diagonals per staged chunk
+constexpr int kDiagStages = 3;  // chunks in flight per thread
+constexpr int kDiagPtrs = 512;  // diagonal pointers staged in shared memory (giant x baby)
+template <int MB>
+constexpr size_t diag_smem() {
+  return (size_t)(2 * MB + kDiagStages * kDiagKL) * diag_threads<MB>() * 8 + kDiagPtrs * 8;
+}
+
+// Memory-level parallelism without barriers: every thread only ever reads the
+// shared-memory words its own cp.async wrote (its coefficient's column), so
+// the baby inputs (u_k, v_k) and the diagonal stream are plain 8-byte async
+// copies -- all baby inputs at once, the diagonals kDiagStages chunks ahead
+// of the multiply-accumulate -- and no __syncthreads is needed anywhere.
 template <int MB>
 __global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArgs a) {
   constexpr int NT = diag_threads<MB>();
-  // baby inputs of this thread's coefficient, u then v (thread-private columns:
-  // shared memory only keeps them out of the register file)
-  __shared__ u64 xs[2 * MB][NT];
+  constexpr int KL = kDiagKL, NS = kDiagStages;
+  extern __shared__ __align__(16) u64 dsm[];
+  u64 (*xs)[NT] = (u64 (*)[NT])dsm;                          // [2 MB][NT] baby inputs
+  u64 (*ds)[KL][NT] = (u64 (*)[KL][NT])(dsm + 2 * MB * NT);  // [NS][KL][NT] diagonals
+  const u64** dps = (const u64**)(dsm + (2 * MB + NS * KL) * NT);  // [giant][baby] diagonal rows
   const int n = 1 << a.logn;
   const int c = blockIdx.x * NT + threadIdx.x;
   const int i = blockIdx.y;
-  if (c >= n) return;
   const int t = threadIdx.x;
+  // the diagonal pointers, once per CTA (a cp.async whose address waits on a
+  // global pointer load stalls the whole stream)
+  const bool staged = a.diag_ptrs && a.giant * a.baby <= kDiagPtrs;
+  if (staged) {
+    for (int e = t; e < a.giant * a.baby; e += NT)
+      dps[e] = a.diag_ptrs[(long long)(e / a.baby) * a.diag_stride + e % a.baby];
+    __syncthreads();
+  }
+  if (c >= n) return;
   const PrimeConst& P = a.pc[a.prime[i]];
   const long long rowN = (long long)a.R << a.logn;
   const long long off = ((long long)i << a.logn) + c;
+  const int nk = (a.baby + KL - 1) / KL;   // chunks per giant group
+  const int nq = a.giant * nk;             // chunks in all
+  auto stage = [&](int q) {                // one commit group per chunk (possibly empty)
+    if (q < nq) {
+      const int s = q % NS, j = q / nk, k1 = (q % nk) * KL;
+      const long long dj = (long long)j * a.diag_stride;
+#pragma unroll
+      for (int kk = 0; kk < KL; ++kk) {
+        const int k = k1 + kk;
+        if (k < a.baby)
+          cp_async8(&ds[s][kk][t], staged ? dps[j * a.baby + k] + off
+                                   : a.diag_ptrs ? a.diag_ptrs[dj + k] + off
+                                                 : a.diags + (dj + k) * rowN + off);
+      }
+    }
+    cp_async_commit();
+  };
+  // baby inputs: all in flight at once (group 0), then the first diagonal chunks
 #pragma unroll
   for (int k = 0; k < MB; ++k) {
     if (k < a.baby) {
-      xs[2 * k][t] = a.uv[(2LL * k) * rowN + off];
-      u64 v = a.uv[(2LL * k + 1) * rowN + off];
-      if (i < a.l) {
-        const u64 g = a.galois[k];
-        const u64 bv = a.b[((long long)i << a.logn) + automorph_src((u32)c, (u32)g, a.logn)];
-        const ulonglong2 pm = a.pmod[i];
-        v = addmod(v, shoup(bv, pm.x, pm.y, P.q), P.q);
-      }
-      xs[2 * k + 1][t] = v;
+      cp_async8(&xs[2 * k][t], a.uv + (2LL * k) * rowN + off);
+      cp_async8(&xs[2 * k + 1][t], a.uv + (2LL * k + 1) * rowN + off);
     }
   }
-  for (int j = 0; j < a.giant; ++j) {
-    const long long dj = (long long)j * a.diag_stride;
-    u64* au = a.acc + (2LL * j) * rowN + off;
-    u64* av = a.acc + (2LL * j + 1) * rowN + off;
-    u64 yu = a.accumulate ? *au : 0, yv = a.accumulate ? *av : 0;
-    // every diagonal of this giant group is requested before the first MAC
-    constexpr int KL = MB < 16 ? MB : 16;
+  cp_async_commit();
 #pragma unroll
-    for (int k1 = 0; k1 < MB; k1 += KL) {
-    if (k1 >= a.baby) continue;
-    u64 m[KL];
+  for (int q = 0; q < NS - 1; ++q) stage(q);
+  // pmodup(automorph(b, t_k)) for the v inputs (chain rows): gathers in registers
+  u64 bv[MB];
+  const bool chain = i < a.l;
+  if (chain) {
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+      if (k < a.baby)
+        bv[k] = a.b[((long long)i << a.logn) + automorph_src((u32)c, (u32)a.galois[k], a.logn)];
+  }
+  cp_async_wait<NS - 1>();  // group 0 (baby inputs) has landed
+  if (chain) {
+    const ulonglong2 pm = a.pmod[i];
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+      if (k < a.baby) xs[2 * k + 1][t] = addmod(xs[2 * k + 1][t], shoup(bv[k], pm.x, pm.y, P.q), P.q);
+  }
+  u64 yu = 0, yv = 0;
+#pragma unroll 1
+  for (int q = 0; q < nq; ++q) {
+    const int s = q % NS, j = q / nk, k1 = (q % nk) * KL;
+    stage(q + NS - 1);          // refills the stage chunk q-1 used
+    cp_async_wait<NS - 1>();    // chunk q has landed
+    if (k1 == 0) {
+      yu = a.accumulate ? a.acc[(2LL * j) * rowN + off] : 0;
+      yv = a.accumulate ? a.acc[(2LL * j + 1) * rowN + off] : 0;
+    }
+    Acc3 su, sv;
+    acc3_zero(su);
+    acc3_zero(sv);
 #pragma unroll
     for (int kk = 0; kk < KL; ++kk) {
       const int k = k1 + kk;
-      m[kk] = k < a.baby ? __ldg(a.diag_ptrs ? a.diag_ptrs[dj + k] + off : a.diags + (dj + k) * rowN + off)
-                         : 0;
-    }
-#pragma unroll
-    for (int k0 = k1; k0 < k1 + KL; k0 += 8) {
-      if (k0 >= a.baby) continue;
-      Acc3 su, sv;
-      acc3_zero(su);
-      acc3_zero(sv);
-#pragma unroll
-      for (int kk = 0; kk < 8 && k0 + kk < MB; ++kk) {
-        const int k = k0 + kk;
-        if (k < a.baby) {
-          const u32 m0 = lo30(m[k - k1]), m1 = hi30(m[k - k1]);
-          const u64 xu = xs[2 * k][t], xv = xs[2 * k + 1][t];
-          acc3_mac(su, m0, m1, lo30(xu), hi30(xu));
-          acc3_mac(sv, m0, m1, lo30(xv), hi30(xv));
-        }
+      if (k < a.baby) {
+        const u64 mv = ds[s][kk][t];
+        const u32 m0 = lo30(mv), m1 = hi30(mv);
+        const u64 xu = xs[2 * k][t], xv = xs[2 * k + 1][t];
+        acc3_mac(su, m0, m1, lo30(xu), hi30(xu));
+        acc3_mac(sv, m0, m1, lo30(xv), hi30(xv));
       }
-      yu = addmod(yu, acc3_reduce(su, P), P.q);
-      yv = addmod(yv, acc3_reduce(sv, P), P.q);
     }
+    yu = addmod(yu, acc3_reduce(su, P), P.q);
+    yv = addmod(yv, acc3_reduce(sv, P), P.q);
+    if (k1 + KL >= a.baby) {   // last chunk of giant group j
+      a.acc[(2LL * j) * rowN + off] = yu;
+      a.acc[(2LL * j + 1) * rowN + off] = yv;
     }
-    *au = yu;
-    *av = yv;
   }
 }
 
@@ -97,9 +141,19 @@ int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
   if (a.baby < 1 || a.baby > kMaxBaby || a.giant < 1 || a.diag_stride < a.baby) return CK_ERR_ARG;
   count_launches(1);
   const int n = 1 << a.logn;
-#define CK_DIAG(MB)                                                                    \
-  diag_mac_kernel<MB><<<dim3((n + diag_threads<MB>() - 1) / diag_threads<MB>(), a.R),       \
-                        diag_threads<MB>(), 0, st>>>(a)
+#define CK_DIAG(MB)                                                                          \
+  do {                                                                                        \
+    static unsigned done = 0;                                                                 \
+    int dev = 0;                                                                              \
+    cudaGetDevice(&dev);                                                                      \
+    if (dev >= 32 || !((done >> dev) & 1u)) {                                                 \
+      cudaFuncSetAttribute(diag_mac_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           (int)diag_smem<MB>());                                             \
+      if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);                    \
+    }                                                                                         \
+    diag_mac_kernel<MB><<<dim3((n + diag_threads<MB>() - 1) / diag_threads<MB>(), a.R),      \
+                          diag_threads<MB>(), diag_smem<MB>(), st>>>(a);                      \
+  } while (0)
   if (a.baby <= 4) CK_DIAG(4);
   else if (a.baby <= 8) CK_DIAG(8);
   else if (a.baby <= 16) CK_DIAG(16);

@@ -158,7 +158,7 @@ struct LevelTab {
 struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
-  bool kc = false;    // chain-row KSKIP+ModDown kernel (CKB200_KC=1; measured slower, see DESIGN)
+  int md_group = 4;   // md_row items per CTA (CKB200_MD_G)
   int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
@@ -619,6 +619,52 @@ int moddown_core(const ck_plan* p, const ModDownTab& m, u64* x, long long xb, u6
                   false, st);
 }
 
+// ModDown of B (u, v) pairs laid out [B][2][R][N] (v at +R N) into out_a, out_b
+// [B][keep][N] with the fused kernels: INTT of the dropped rows (row + column
+// phase), centered BC, forward column phase of the converted rows, then md_row
+// (their forward row phase + (x - conv) P^-1 + addends, u and v in one launch).
+// addend_v: added to v after the automorphism by gal[b] (or gt); addend_u /
+// add_scale: relinearisation's pmodup terms (see keyswitch_fused).
+int moddown_pairs(const ck_plan* p, const ModDownTab& m, u64* x, long long R, u64* conv, int B,
+                  u64* out_a, u64* out_b, const u64* addend_v, const u64* addend_u,
+                  const ulonglong2* add_scale, long long add_batch, u64 gt, const u64* gal,
+                  cudaStream_t st) {
+  const long long N = p->n, keep = m.keep;
+  CK_TRY(ntt_phase(p, x, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
+                   true, 0, st));
+  const ck::BconvArgs g1 = bconv_args(p, m.bc, x + (long long)m.drop_row0 * N, R * N, conv,
+                                      keep * N, false);
+  CK_TRY(ck::launch_bconv(g1, 2 * B, st));
+  CK_TRY(ntt_phase(p, conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, keep * N, false, 1,
+                   st));
+  ck::MdRowArgs ma{};
+  ma.prime = m.d_keep_prime;
+  ma.pinv = m.d_pinv;
+  ma.pc = p->d_pc;
+  ma.tw = p->d_tw;
+  ma.logn = p->logn;
+  ma.x = x;
+  ma.x_batch = 2 * R * N;
+  ma.conv = conv;
+  ma.conv_batch = 2 * keep * N;
+  ma.addend = addend_v;
+  ma.addend_u = addend_u;
+  ma.add_scale = add_scale;
+  ma.addend_batch = add_batch;
+  ma.out = out_a;
+  ma.out_batch = keep * N;
+  ma.galois = gal;
+  ma.galois_t = gt;
+  ma.pair = 1;
+  ma.x_w = R * N;
+  ma.conv_w = keep * N;
+  ma.out2 = out_b;
+  ma.lazy = 1;
+  for (int k = 0; k < keep; ++k) ma.lazy &= p->mod[k] < ((u64)1 << 59) ? 1 : 0;
+  ma.group = p->md_group;
+  return ck::launch_md_row(ma, (int)keep, B, st);
+}
+
 // Fused key-switch of a batch (see fused.cu): ModUp (INTT row + column phase,
 // BC, forward column phase), ks_row (digit row phases + automorphism + KSKIP),
 // ModDown (INTT of the dropped rows, centered BC, forward column phase) and
@@ -689,11 +735,8 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
   ka_.R = (int)R;
   ka_.logn = p->logn;
   ka_.key_prefetch = p->key_prefetch;
-  // chain-row kernel: ks_row only produces the rows ModDown drops (specials, and
-  // q_last for relinearisation); the kept rows' KSKIP runs inside kc_row below
-  const bool kc = p->kc && t.beta <= 4;
-  ka_.row0 = kc ? (int)keep : 0;
-  CK_TRY(ck::launch_ks_row(ka_, (int)(R - ka_.row0), B, st));
+  ka_.row0 = 0;
+  CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   if (relin) {
     // pmodup (ckks.py:478-489) on the dropped chain row q_last: it feeds the BC
     const int* lp = t.d_chain_prime + (l - 1);
@@ -704,83 +747,10 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
                   2 * R * N, relin->c3 + (l - 1) * N, l * N, nullptr, 0, lp, pm, 1, nullptr, 1, B,
                   st));
   }
-  // ---- ModDown: INTT of the dropped rows, centered BC, fwd column phase
-  CK_TRY(ntt_phase(p, w.uv, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
-                   true, 0, st));
-  {
-    const ck::BconvArgs g1 = bconv_args(p, m.bc, w.uv + (long long)m.drop_row0 * N, R * N, w.conv,
-                                        keep * N, false);
-    CK_TRY(ck::launch_bconv(g1, 2 * B, st));
-    CK_TRY(ntt_phase(p, w.conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, keep * N, false,
-                     1, st));
-  }
-  if (kc) {
-    // ---- kept chain rows: KSKIP + fwd row phase of the converted rows + epilogue, one launch
-    ck::KcRowArgs kr{};
-    kr.a_eval = a_src;
-    kr.a_batch = l * N;
-    kr.dig = w.dig;
-    kr.dig_batch = dig_b;
-    kr.key_b = keys.b;
-    kr.key_a = keys.a;
-    kr.key_b_ptrs = keys.bp;
-    kr.key_a_ptrs = keys.ap;
-    kr.key_digit_stride = ka_.key_digit_stride;
-    kr.key_batch = ka_.key_batch;
-    kr.prime = t.d_raised_prime;  // kept rows j < keep: raised row j == chain row j
-    kr.pc = p->d_pc;
-    kr.tw = p->d_tw;
-    kr.galois = kgal;
-    kr.galois_t = kgt;
-    for (int d = 0; d < 16; ++d) {
-      kr.lo[d] = ka_.lo[d];
-      kr.hi[d] = ka_.hi[d];
-    }
-    kr.beta = t.beta;
-    kr.R = (int)R;
-    kr.logn = p->logn;
-    kr.key_prefetch = p->key_prefetch;
-    kr.conv = w.conv;
-    kr.conv_batch = 2 * keep * N;
-    kr.conv_w = keep * N;
-    kr.pinv = m.d_pinv;
-    kr.add_u = relin ? relin->b3 : nullptr;
-    kr.add_v = relin ? relin->c3 : b_add;
-    kr.add_batch = l * N;
-    kr.add_scale = relin ? m.d_dinv : nullptr;
-    kr.egalois = relin ? nullptr : egal;
-    kr.egalois_t = relin ? 1 : egt;
-    kr.out_a = out_a;
-    kr.out_b = out_b;
-    kr.out_batch = keep * N;
-    return ck::launch_kc_row(kr, (int)keep, B, st);
-  }
-  // ---- fwd row phase of the converted rows fused with the epilogue (u and v in one launch)
-  ck::MdRowArgs ma{};
-  ma.prime = m.d_keep_prime;
-  ma.pinv = m.d_pinv;
-  ma.pc = p->d_pc;
-  ma.tw = p->d_tw;
-  ma.logn = p->logn;
-  ma.x = w.uv;
-  ma.x_batch = 2 * R * N;
-  ma.conv = w.conv;
-  ma.conv_batch = 2 * keep * N;
-  ma.addend = relin ? relin->c3 : b_add;
-  ma.addend_u = relin ? relin->b3 : nullptr;
-  ma.add_scale = relin ? m.d_dinv : nullptr;
-  ma.addend_batch = l * N;
-  ma.out = out_a;
-  ma.out_batch = keep * N;
-  ma.galois = relin ? nullptr : egal;
-  ma.galois_t = relin ? 1 : egt;
-  ma.pair = 1;
-  ma.x_w = R * N;
-  ma.conv_w = keep * N;
-  ma.out2 = out_b;
-  ma.lazy = 1;
-  for (int k = 0; k < keep; ++k) ma.lazy &= p->mod[k] < ((u64)1 << 59) ? 1 : 0;
-  return ck::launch_md_row(ma, (int)keep, B, st);
+  // ---- ModDown pair (fused): INTT, BC, column phase, md_row epilogue
+  return moddown_pairs(p, m, w.uv, R, w.conv, B, out_a, out_b, relin ? relin->c3 : b_add,
+                       relin ? relin->b3 : nullptr, relin ? m.d_dinv : nullptr, l * N,
+                       relin ? 1 : egt, relin ? nullptr : egal, st);
 }
 
 }  // namespace
@@ -821,8 +791,7 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
   {
     const char* e = getenv("CKB200_UNFUSED");
     p->fused = !(e && e[0] == '1');
-    const char* kc = getenv("CKB200_KC");
-    p->kc = kc && kc[0] == '1';
+    if (const char* mg = getenv("CKB200_MD_G")) p->md_group = std::max(1, atoi(mg));
     const char* tc = getenv("CKB200_BCTC");
     if (tc) p->bc_tc = atoi(tc);
   }
@@ -1170,6 +1139,9 @@ int ck_hrotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
   CK_TRY(kskip_impl(p, level, dig, keys, 1, gal, uv, uv + R * N, 2 * R * N, n_rot, st, true));
   // ModDown pair of every rotation (ckks.py:664-666): b is shared, gathered
   // with each rotation's Galois element
+  if (ck::fused_supported(p->logn) && p->fused)
+    return moddown_pairs(p, m, uv, R, conv, n_rot, out_a, out_b, b, nullptr, nullptr, 0, 1, gal,
+                         st);
   CK_TRY(moddown_core(p, m, uv, R * N, conv, 2 * n_rot, st));
   CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, l * N, uv, 2 * R * N, conv, 2 * l * N, nullptr, 0,
                 m.d_keep_prime, m.d_pinv, 1, nullptr, level, n_rot, st));
@@ -1248,6 +1220,9 @@ int ck_pt_matvec(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
     CK_TRY(ck::launch_diag_mac(da, st));
   }
   // one merged ModDown pair by P * q_last (ckks.py:712-717)
+  if (ck::fused_supported(p->logn) && p->fused)
+    return moddown_pairs(p, m, acc, R, conv, 1, out_a, out_b, nullptr, nullptr, nullptr, 0, 1,
+                         nullptr, st);
   CK_TRY(moddown_core(p, m, acc, R * N, conv, 2, st));
   CK_TRY(ew_run(p, ck::EW_MODDOWN, out_a, 0, acc, 0, conv, 0, nullptr, 0, m.d_keep_prime, m.d_pinv,
                 1, nullptr, (int)lo, 1, st));
@@ -1324,11 +1299,16 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
     CK_TRY(ck::launch_diag_mac(da, st));
   }
   // 4. merged ModDown (P * q_last) of every accumulator -> level l-1
-  CK_TRY(moddown_core(p, m, acc, R * N, conv, 2 * giant, st));
-  CK_TRY(ew_run(p, ck::EW_MODDOWN, ga, lo * N, acc, 2 * R * N, conv, 2 * lo * N, nullptr, 0,
-                m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
-  CK_TRY(ew_run(p, ck::EW_MODDOWN, gb, lo * N, acc + R * N, 2 * R * N, conv + lo * N, 2 * lo * N,
-                nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
+  if (ck::fused_supported(p->logn) && p->fused) {
+    CK_TRY(moddown_pairs(p, m, acc, R, conv, giant, ga, gb, nullptr, nullptr, nullptr, 0, 1,
+                         nullptr, st));
+  } else {
+    CK_TRY(moddown_core(p, m, acc, R * N, conv, 2 * giant, st));
+    CK_TRY(ew_run(p, ck::EW_MODDOWN, ga, lo * N, acc, 2 * R * N, conv, 2 * lo * N, nullptr, 0,
+                  m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
+    CK_TRY(ew_run(p, ck::EW_MODDOWN, gb, lo * N, acc + R * N, 2 * R * N, conv + lo * N, 2 * lo * N,
+                  nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, giant, st));
+  }
   // 5. giant rotations at l-1, batched
   CK_TRY(rotate_impl(p, ga, gb, gkeys, (int)lo, 1, ggal, 0, ra, rb, rws, giant, st));
   // 6. sum of the rotated giants

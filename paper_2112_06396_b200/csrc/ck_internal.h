@@ -92,42 +92,7 @@ struct KsRowArgs {
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
 
-// Chain-row key-switch kernel (fused.cu kc_row_kernel): for every KEPT chain
-// row j, KSKIP (digit row phases + automorphism + MAC with both key rows) AND
-// the ModDown epilogue (forward row phase of the converted rows, (x - conv) *
-// P^-1, + addends) in one pass: u/v chain rows never touch HBM.
-struct KcRowArgs {
-  const u64* a_eval;            // [B][l][N] eval input (own digit rows)
-  long long a_batch;
-  const u64* dig;               // [B][beta][R][N] ModUp targets after the column phase
-  long long dig_batch;
-  const u64* key_b;
-  const u64* key_a;
-  long long key_digit_stride, key_batch;
-  const u64* const* key_b_ptrs;
-  const u64* const* key_a_ptrs;
-  const int* prime;             // [keep] prime index of chain row j (== key row j)
-  const PrimeConst* pc;
-  const ulonglong2* tw;
-  const u64* galois;            // KSKIP automorphism per batch item (nullable: galois_t)
-  u64 galois_t;
-  int lo[16], hi[16];           // digit spans (chain rows)
-  int beta, R, logn;
-  int key_prefetch;
-  const u64* conv;              // [B][2][keep][N] converted rows after the column phase
-  long long conv_batch, conv_w;
-  const ulonglong2* pinv;       // [keep] ModDown P^-1 (Shoup)
-  const u64* add_u;             // nullable [B][.][N]: added to out_a (times add_scale)
-  const u64* add_v;             // nullable: added to out_b, gathered with egalois
-  long long add_batch;
-  const ulonglong2* add_scale;  // nullable [keep]
-  const u64* egalois;           // addend automorphism per batch item (nullable: egalois_t)
-  u64 egalois_t;
-  u64* out_a;
-  u64* out_b;
-  long long out_batch;
-};
-int launch_kc_row(const KcRowArgs& a, int rows, int batch, cudaStream_t st);
+
 #ifdef __CUDACC__
 // base of batch item b's key block: pointer array when given, else base + b * stride
 __device__ __forceinline__ const u64* key_block(const u64* base, const u64* const* ptrs,
@@ -160,6 +125,8 @@ struct MdRowArgs {
   long long x_w, conv_w;
   u64* out2;
   int lazy;                     // every kept prime < 2^59: conv stays lazy (md_row_kernel<.., true>)
+  int group;                    // items (batch x {u,v}) per CTA, same limb and rows (L1 twiddle reuse)
+  int batch;                    // set by launch_md_row
 };
 int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st);
 

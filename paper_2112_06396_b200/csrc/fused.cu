@@ -280,9 +280,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
   __shared__ u64 stage[F::TR * F::RS];
-  const int j = blockIdx.z;  // grid (row tile, batch, limb): twiddle reuse across the batch
-  const int w = a.pair ? (blockIdx.y & 1) : 1;   // w = 1: the polynomial that gets the addend
-  const long long b = a.pair ? (blockIdx.y >> 1) : blockIdx.y;
+  const int j = blockIdx.z;  // grid (row tile, item group, limb)
   const int prime = a.prime[j];
   const PrimeConst& P = a.pc[prime];
   const u64 q = P.q, two_q = P.two_q;
@@ -294,6 +292,14 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   const long long ro = ((long long)j << LOGN) + ((long long)r << P2);
   pdl_trigger();
   pdl_wait();
+  // a CTA runs `group` consecutive items (batch x {u, v}) of the SAME limb and
+  // rows: the row twiddles come from L1 after the first item
+  const int items = a.pair ? 2 * a.batch : a.batch;
+  const int i_end = min(items, ((int)blockIdx.y + 1) * a.group);
+#pragma unroll 1
+  for (int item = blockIdx.y * a.group; item < i_end; ++item) {
+  const int w = a.pair ? (item & 1) : 1;   // w = 1: the polynomial that gets the addend
+  const long long b = a.pair ? (item >> 1) : item;
   const u64* conv = a.conv + b * a.conv_batch + ro + (a.pair && w ? a.conv_w : 0);
   const u64* x = a.x + b * a.x_batch + ro + (a.pair && w ? a.x_w : 0);
   u64 y[kE];
@@ -343,189 +349,8 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
              ((long long)r << P2);
 #pragma unroll
   for (int k = 0; k < kE; ++k) out[sub_index<P2, 0, false>(g, k)] = o[k];
-}
-
-// ------------------------------------------------------- KSKIP + ModDown (chain rows)
-// One CTA = kept chain row j x TR storage rows x one batch item:
-//   slots 0..BETA-1: the digits' source rows sigma(r) (cp.async, own digit from
-//     the input), forward row phase in place (as ks_row_kernel);
-//   conv_u row r -> registers, forward row phase (slot BETA = exchange buffer):
-//     thread g of a row ends up owning columns 16 g + k (k = 0..15);
-//   u(r, c) = sum_d digit_d[sigma(r)][pi_r(c)] * key_a[d][j][r, c]   (_kskip on
-//     automorph'ed digits, ckks.py:450-465, 663), out_a = (u - conv_u) * P^-1
-//     [+ add_u * scale]                                     (ckks.py:411-416)
-//   then the same for v with key_b and conv_v, + automorph(add_v) (ckks.py:664-666).
-// u and v exist only in registers: the chain rows' KSKIP output never touches HBM.
-#ifndef CKB200_KC_EPC
-#define CKB200_KC_EPC 2048
-#endif
-#ifndef CKB200_KC_MINB
-#define CKB200_KC_MINB 4
-#endif
-constexpr int kKcEpc = CKB200_KC_EPC;
-
-// MAC + ModDown epilogue of one polynomial (u: V = false, v: V = true) over the
-// CTA's contiguous TR x S tile in the coalesced MAC mapping of ks_row_kernel:
-// thread t owns element pairs e = 2t + 2 NT m; digits and the converted row
-// (natural order, lazy [0, 16q)) come from shared memory.
-template <int P2, int LOGN, int BETA, bool V>
-__device__ __forceinline__ void kc_mac_epilogue(const KcRowArgs& a, const u64* fsm, int j,
-                                                long long b, u64 t, const PrimeConst& P,
-                                                ulonglong2 pinv, const u64* key, u64* out,
-                                                int own, const u64* arow) {
-  using F = FusedCfg<P2, kKcEpc>;
-  constexpr int SLOT = F::TR * F::RS;
-  constexpr int ITER = (F::TR * F::S) / (2 * F::NT);
-  const u64 q = P.q;
-  const u64* add = V ? a.add_v : a.add_u;
-  const ulonglong2 asc = a.add_scale ? a.add_scale[j] : make_ulonglong2(0, 0);
-  const u64 te = V ? (a.egalois ? a.egalois[b] : a.egalois_t) : 1;
-  const long long tile0 = (long long)blockIdx.x * F::TR << P2;
-  const u64* addrow = add ? add + b * a.add_batch + ((long long)j << LOGN) : nullptr;
-  const u64* kt = key + tile0;
-  u64* ot = out + ((long long)j << LOGN) + tile0;
-  const u64* cs = fsm + (BETA - 1) * SLOT;  // converted row (slots 0..BETA-2: non-own digits)
-  ulonglong2 kv[BETA];
-#pragma unroll
-  for (int d = 0; d < BETA; ++d)
-    kv[d] = __ldg((const ulonglong2*)(kt + d * a.key_digit_stride + 2 * (int)threadIdx.x));
-#pragma unroll 1
-  for (int m = 0; m < ITER; ++m) {
-    const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
-    ulonglong2 kn[BETA];
-    if (m + 1 < ITER) {
-#pragma unroll
-      for (int d = 0; d < BETA; ++d)
-        kn[d] = __ldg((const ulonglong2*)(kt + d * a.key_digit_stride + e + 2 * F::NT));
-    }
-    const int er = e >> P2, ec = e & (F::S - 1);
-    const u32 eg = (u32)(tile0 + e);  // limb-global storage index of element 0 of the pair
-    u64 o[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const u32 src = t == 1 ? eg + h : automorph_src(eg + h, (u32)t, LOGN);
-      const int sc = (int)(src & (F::S - 1));
-      Acc3 acc;
-      acc3_zero(acc);
-#pragma unroll
-      for (int d = 0; d < BETA; ++d) {
-        // the row's own digit is the input row itself (ckks.py:439): gathered from
-        // global memory (L1), the others from their shared-memory slots
-        const u64 x = d == own ? __ldg(arow + src)
-                               : fsm[(d - (d > own)) * SLOT + er * F::RS + sidx(sc)];
-        const u64 kx = h ? kv[d].y : kv[d].x;
-        acc3_mac(acc, lo30(x), hi30(x), lo30(kx), hi30(kx));
-      }
-      const u64 u = acc3_reduce(acc, P);
-      u64 v = shoup(u + (q << 4) - cs[er * F::RS + sidx(ec + h)], pinv.x, pinv.y, q);
-      if (addrow) {
-        const u64 z = __ldg(addrow + (te == 1 ? eg + h : automorph_src(eg + h, (u32)te, LOGN)));
-        v = addmod(v, a.add_scale ? shoup(z, asc.x, asc.y, q) : z, q);
-      }
-      o[h] = v;
-    }
-    *(ulonglong2*)(ot + e) = make_ulonglong2(o[0], o[1]);
-    if (m + 1 < ITER) {
-#pragma unroll
-      for (int d = 0; d < BETA; ++d) kv[d] = kn[d];
-    }
+  __syncthreads();  // srow is the next item's exchange buffer
   }
-}
-
-template <int P1, int P2, int BETA>
-__global__ void __launch_bounds__(FusedCfg<P2, kKcEpc>::NT, CKB200_KC_MINB) kc_row_kernel(KcRowArgs a) {
-  using F = FusedCfg<P2, kKcEpc>;
-  constexpr int LOGN = P1 + P2;
-  constexpr int SLOT = F::TR * F::RS;
-  static_assert(F::G * kE == F::S, "row layout");
-  extern __shared__ __align__(16) u64 fsm[];
-  pdl_trigger();
-  const int j = blockIdx.z;            // kept chain row (== key row)
-  const long long b = blockIdx.y;
-  const int prime = a.prime[j];
-  const PrimeConst& P = a.pc[prime];
-  const u64 q = P.q, two_q = P.two_q;
-  const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
-  const int r = blockIdx.x * F::TR + rl;
-  const u64 t = a.galois ? a.galois[b] : a.galois_t;
-  const int sr = t == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)t, LOGN) >> P2);
-  const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
-  const ulonglong2 pinv = a.pinv[j];
-  const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN);
-  const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN);
-  const long long tile0 = (long long)blockIdx.x * F::TR << P2;
-  // L2 prefetch (bulk, no registers): the key_a tiles and the own digit's source
-  // rows now (used by the u MAC), the key_b tiles and addend rows later
-  if (threadIdx.x < BETA)
-    prefetch_l2(ka + threadIdx.x * a.key_digit_stride + tile0, F::TR * F::S * 8);
-  int own = 0;  // the digit whose span holds chain row j: its row is the input itself
-#pragma unroll
-  for (int d = 0; d < BETA; ++d)
-    if (j >= a.lo[d] && j < a.hi[d]) own = d;
-  const u64* arow = a.a_eval + b * a.a_batch + ((long long)j << LOGN);
-  pdl_wait();  // digits, conv and the ciphertext rows are the predecessors' output
-  if (g == 0) prefetch_l2(arow + ((long long)sr << P2), F::S * 8);
-  constexpr int NS = BETA - 1;  // non-own digits, one shared-memory slot each
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int d = s + (s >= own);
-    const u64* src = a.dig + b * a.dig_batch + ((long long)(d * a.R + j) << LOGN) +
-                     ((long long)sr << P2);
-    u64* srow = fsm + s * SLOT + rl * F::RS;
-#pragma unroll
-    for (int k = 0; k < kE; ++k) {
-      const int s0 = sub_index<P2, 0, false>(g, k);
-      cp_async8(srow + sidx(s0), src + s0);
-    }
-    cp_async_commit();
-  }
-  const u64* conv = a.conv + b * a.conv_batch + ((long long)j << LOGN) + ((long long)r << P2);
-  u64 y[kE];
-#pragma unroll
-  for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    u64* srow = fsm + s * SLOT + rl * F::RS;
-    if (s == 0) cp_async_wait<(NS >= 1 ? NS - 1 : 0)>();
-    else if (s == 1) cp_async_wait<(NS >= 2 ? NS - 2 : 0)>();
-    else cp_async_wait<0>();
-    ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);
-  }
-  u64* xrow = fsm + NS * SLOT + rl * F::RS;
-  // conv_u forward row phase (its internal barriers also publish the digit slots),
-  // natural order into slot BETA
-  row_transform<P2, false, LOGN>(y, g, r << P2, xrow, tw, q, two_q);
-  if (q >= (1ull << 59)) {  // keep u + 16q - conv below 2^64
-#pragma unroll
-    for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
-  }
-  __syncthreads();
-  row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, xrow);
-  // conv_v's input rows are requested before the u MAC
-  const u64* convv = conv + a.conv_w;
-#pragma unroll
-  for (int k = 0; k < kE; ++k) y[k] = convv[sub_index<P2, 0, false>(g, k)];
-  __syncthreads();
-  if (threadIdx.x < BETA)
-    prefetch_l2(kb + threadIdx.x * a.key_digit_stride + tile0, F::TR * F::S * 8);
-  if (a.add_v && g == 0) {
-    const u64 te = a.egalois ? a.egalois[b] : a.egalois_t;
-    const int se = te == 1 ? r : (int)(automorph_src((u32)r << P2, (u32)te, LOGN) >> P2);
-    prefetch_l2(a.add_v + b * a.add_batch + ((long long)j << LOGN) + ((long long)se << P2), F::S * 8);
-  }
-  kc_mac_epilogue<P2, LOGN, BETA, false>(a, fsm, j, b, t, P, pinv, ka, a.out_a + b * a.out_batch,
-                                         own, arow);
-  // conv_v: row_transform's first barrier orders its slot writes after the u MAC's reads
-  row_transform<P2, false, LOGN>(y, g, r << P2, xrow, tw, q, two_q);
-  if (q >= (1ull << 59)) {
-#pragma unroll
-    for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
-  }
-  __syncthreads();
-  row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, xrow);
-  __syncthreads();
-  kc_mac_epilogue<P2, LOGN, BETA, true>(a, fsm, j, b, t, P, pinv, kb, a.out_b + b * a.out_batch,
-                                        own, arow);
 }
 
 // ------------------------------------------------------------------ launch
@@ -558,57 +383,14 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
 template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2>;
-  const dim3 grid((1 << P1) / F::TR, batch * (a.pair ? 2 : 1), rows);
-  if (a.lazy) launch_pdl(md_row_kernel<P1, P2, true>, grid, dim3(F::NT), 0, st, a);
-  else launch_pdl(md_row_kernel<P1, P2, false>, grid, dim3(F::NT), 0, st, a);
+  MdRowArgs g = a;
+  g.batch = batch;
+  const int items = batch * (a.pair ? 2 : 1);
+  if (g.group < 1) g.group = 1;
+  const dim3 grid((1 << P1) / F::TR, (items + g.group - 1) / g.group, rows);
+  if (a.lazy) launch_pdl(md_row_kernel<P1, P2, true>, grid, dim3(F::NT), 0, st, g);
+  else launch_pdl(md_row_kernel<P1, P2, false>, grid, dim3(F::NT), 0, st, g);
   return 0;
-}
-
-template <int P1, int P2, int BETA>
-static void launch_kc_row_b(const KcRowArgs& a, int rows, int batch, cudaStream_t st) {
-  using F = FusedCfg<P2, kKcEpc>;
-  const size_t smem = (size_t)BETA * F::TR * F::RS * 8;  // BETA-1 digit slots + the converted row
-  auto kern = kc_row_kernel<P1, P2, BETA>;
-  if (smem > 48 * 1024) {
-    static std::atomic<unsigned> done{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const unsigned bit = dev < 32 ? 1u << dev : 0u;
-    if (!bit || !(done.load(std::memory_order_relaxed) & bit)) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      done.fetch_or(bit, std::memory_order_relaxed);
-    }
-  }
-  launch_pdl(kern, dim3((1 << P1) / F::TR, batch, rows), dim3(F::NT), smem, st, a);
-}
-
-template <int P1, int P2>
-static int launch_kc_row_t(const KcRowArgs& a, int rows, int batch, cudaStream_t st) {
-  switch (a.beta) {
-    case 1: launch_kc_row_b<P1, P2, 1>(a, rows, batch, st); break;
-    case 2: launch_kc_row_b<P1, P2, 2>(a, rows, batch, st); break;
-    case 3: launch_kc_row_b<P1, P2, 3>(a, rows, batch, st); break;
-    case 4: launch_kc_row_b<P1, P2, 4>(a, rows, batch, st); break;
-    default: return CK_ERR_ARG;
-  }
-  return 0;
-}
-
-int launch_kc_row(const KcRowArgs& a, int rows, int batch, cudaStream_t st) {
-  if (rows <= 0 || batch <= 0) return 0;
-  int e = 0;
-  switch (a.logn) {
-    case 12: e = launch_kc_row_t<6, 6>(a, rows, batch, st); break;
-    case 13: e = launch_kc_row_t<6, 7>(a, rows, batch, st); break;
-    case 14: e = launch_kc_row_t<7, 7>(a, rows, batch, st); break;
-    case 15: e = launch_kc_row_t<7, 8>(a, rows, batch, st); break;
-    case 16: e = launch_kc_row_t<8, 8>(a, rows, batch, st); break;
-    case 17: e = launch_kc_row_t<8, 9>(a, rows, batch, st); break;
-    default: return CK_ERR_ARG;
-  }
-  if (e) return e;
-  count_launches(1);
-  return (int)cudaGetLastError();
 }
 
 bool fused_supported(int logn) { return logn >= 12 && logn <= 17; }

@@ -136,6 +136,28 @@ CK_D void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// TMA bulk copies (cp.async.bulk, no tensor map): `bytes` (multiple of 16,
+// 16-B aligned) global -> shared, completion counted on an mbarrier.
+CK_D void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count) : "memory");
+}
+CK_D void mbar_expect_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+CK_D void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+               "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+CK_D void mbar_wait_parity(void* bar, unsigned phase) {
+  asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+               "@!P1 bra WAIT_%=;\n\t}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(phase) : "memory");
+}
+
 // Ampere-style async copies (LDGSTS): 8-byte global -> shared, grouped.
 CK_D void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

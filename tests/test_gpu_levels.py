@@ -135,3 +135,34 @@ def test_relin_argument_errors():
                         x.data_ptr(), x.data_ptr(), x.data_ptr(), 1, None) == _lib.CK_ERR_ARG
     assert lib.ck_relin(h, x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(),
                         p.limbs, x.data_ptr(), x.data_ptr(), x.data_ptr(), 0, None) == _lib.CK_ERR_ARG
+
+
+@pytest.mark.parametrize("kind", ["pt_matvec", "bsgs", "hrotate"])
+def test_hoisted_paths_fused_ring_match_oracle(kind):
+    """hrotate / pt_matvec / BSGS at N = 2^12 run the fused ModDown (md_row) path;
+    bit-exact against the oracle (the toy goldens cover the small-ring path)."""
+    p = _params(12, 6, 2, 3)
+    mods, raised = p.chain, p.raised_moduli(p.limbs)
+    a = cases._rows(p, 0, synth.TAG_CT_A, mods)
+    b = cases._rows(p, 0, synth.TAG_CT_B, mods)
+    ob, gb = cases.OracleBackend(), gpu_backend.GpuBackend()
+    if kind == "pt_matvec":
+        offs = (0, 1, 5, -3, 40)
+        diags = {o: cases._rows(p, 0, synth.TAG_DIAG, raised, digit=o % 64) for o in offs}
+        keys = cases._keys(p, [-o for o in offs if o % p.slots])
+        want, got = ob.pt_matvec(p, a, b, keys, diags), gb.pt_matvec(p, a, b, keys, diags)
+    elif kind == "bsgs":
+        baby, giant = 5, 3
+        diags = {(j, k): cases._rows(p, j, synth.TAG_DIAG, raised, digit=k)
+                 for j in range(1, giant + 1) for k in range(1, baby + 1)}
+        rs = sorted({-k for k in range(1, baby + 1)} | {-baby * j for j in range(1, giant + 1)})
+        keys = cases._keys(p, rs)
+        want = ob.bsgs(p, a, b, keys, diags, baby, giant)
+        got = gb.bsgs(p, a, b, keys, diags, baby, giant)
+    else:
+        rots = (1, -2, 7, 100)
+        keys = cases._keys(p, rots)
+        want = [x for pair in ob.hrotate(p, a, b, keys, rots) for x in pair]
+        got = [x for pair in gb.hrotate(p, a, b, keys, rots) for x in pair]
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
