@@ -75,14 +75,67 @@ bool isprime_h(u64 n) {
   return true;
 }
 
+// Pollard-rho (Brent) factor finding: q - 1 for any q < 2^60 factors in
+// milliseconds (trial division to sqrt(q-1) is quadratic-time for unlucky primes)
+u64 rho_factor(u64 n) {
+  if (n % 2 == 0) return 2;
+  for (u64 c = 1;; ++c) {
+    auto f = [&](u64 x) { return (u64)(((u128)x * x + c) % n); };
+    u64 x = 2, y = 2, d = 1, q = 1, ys = 2;
+    const u64 m = 128;
+    u64 r = 1;
+    do {
+      x = y;
+      for (u64 i = 0; i < r; ++i) y = f(y);
+      u64 k = 0;
+      do {
+        ys = y;
+        for (u64 i = 0; i < m && i < r - k; ++i) {
+          y = f(y);
+          q = (u64)((u128)q * (x > y ? x - y : y - x) % n);
+        }
+        u64 a = q, b = n;
+        while (b) { const u64 t = a % b; a = b; b = t; }
+        d = a;
+        k += m;
+      } while (k < r && d == 1);
+      r <<= 1;
+    } while (d == 1);
+    if (d == n) {  // backtrack one step at a time
+      do {
+        ys = f(ys);
+        u64 a = x > ys ? x - ys : ys - x, b = n;
+        while (b) { const u64 t = a % b; a = b; b = t; }
+        d = a;
+      } while (d == 1);
+    }
+    if (d != n) return d;
+  }
+}
+
+void factor_into(u64 m, std::vector<u64>& f) {
+  if (m == 1) return;
+  if (isprime_h(m)) {
+    if (std::find(f.begin(), f.end(), m) == f.end()) f.push_back(m);
+    return;
+  }
+  for (u64 p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull}) {
+    if (m % p == 0) {
+      if (std::find(f.begin(), f.end(), p) == f.end()) f.push_back(p);
+      while (m % p == 0) m /= p;
+      factor_into(m, f);
+      return;
+    }
+  }
+  const u64 d = rho_factor(m);
+  factor_into(d, f);
+  factor_into(m / d, f);
+}
+
 std::vector<u64> prime_factors(u64 m) {
   std::vector<u64> f;
-  if (m % 2 == 0) { f.push_back(2); while (m % 2 == 0) m /= 2; }
-  for (u64 d = 3; d * d <= m; d += 2) {
-    if (m % d == 0) { f.push_back(d); while (m % d == 0) m /= d; }
-    if (m > 1 && isprime_h(m)) break;
-  }
-  if (m > 1) f.push_back(m);
+  factor_into(m, f);
+  std::sort(f.begin(), f.end());
   return f;
 }
 
@@ -605,6 +658,8 @@ int kskip_impl(const ck_plan* p, int l, const u64* digits, const Keys& keys,
   a.galois_t = gt % (2ull * p->n);
   a.beta = t.beta;
   a.logn = p->logn;
+  a.accumulate = 0;
+  a.key_digit0 = 0;
   return ck::launch_kskip(a, t.R, B, st);
 }
 
@@ -1032,7 +1087,7 @@ int rotate_impl(const ck_plan* p, const u64* a, const u64* b, const Keys& keys, 
     egt = 1;
     kgal = nullptr;
   }
-  if (ck::fused_supported(p->logn) && p->fused) {
+  if (ck::fused_supported(p->logn) && p->fused && t.beta <= 8) {
     const u64* egal = mode == 1 ? nullptr : galois;
     return keyswitch_fused(p, level, a_src, b_add, keys, kgt, kgal, egt, egal, nullptr, out_a,
                            out_b, w, batch, st);
@@ -1083,7 +1138,7 @@ int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const u
   const Ws w = ws_layout(p, level, batch, ws);
   Keys keys = keys_block((const u64*)key_b, (const u64*)key_a);
   keys.shared = true;  // one relinearisation key for the whole batch
-  if (ck::fused_supported(p->logn) && p->fused) {
+  if (ck::fused_supported(p->logn) && p->fused && t.beta <= 8) {
     const Relin rl{b3, c3};
     return keyswitch_fused(p, level, a3, nullptr, keys, 1, nullptr, 1, nullptr, &rl, out_a, out_b,
                            w, batch, st);

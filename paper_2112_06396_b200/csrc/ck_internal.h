@@ -197,6 +197,8 @@ struct KskipArgs {
   const u64* galois;            // per batch item Galois element (nullable: galois_t)
   u64 galois_t;                 // 1 = no automorphism
   int beta, logn;
+  int accumulate;               // 1: u += .., v += .. (digit chunks beyond kKsMaxBeta)
+  int key_digit0;               // first key digit of this launch (pointer-array keys)
 };
 int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st);
 

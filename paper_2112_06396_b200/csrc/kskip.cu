@@ -41,8 +41,10 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
   const u64 t = a.galois ? a.galois[bz] : a.galois_t;
   const long long tile0 = (long long)blockIdx.y * TILE;
   const int krow = a.key_row[i];
-  const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, bz) + ((long long)krow << logn);
-  const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, bz) + ((long long)krow << logn);
+  // key_digit0: first digit of this chunk (pointer-array keys point at digit 0)
+  const long long kd0 = a.key_b_ptrs ? (long long)a.key_digit0 * a.key_digit_stride : 0;
+  const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, bz) + kd0 + ((long long)krow << logn);
+  const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, bz) + kd0 + ((long long)krow << logn);
   const u64* dig = a.digits + bz * a.digits_batch + ((long long)i << logn);
   // stage the gathered digit rows: for each storage row in the tile load the
   // source row perm maps it to
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
         acc3_mac(su, x0, x1, lo30(ya[h][d]), hi30(ya[h][d]));
         acc3_mac(sv, x0, x1, lo30(yb[h][d]), hi30(yb[h][d]));
       }
-      uo[o] = acc3_reduce(su, P);
-      vo[o] = acc3_reduce(sv, P);
+      uo[o] = a.accumulate ? addmod(uo[o], acc3_reduce(su, P), P.q) : acc3_reduce(su, P);
+      vo[o] = a.accumulate ? addmod(vo[o], acc3_reduce(sv, P), P.q) : acc3_reduce(sv, P);
     }
     return;
   }
@@ -113,14 +115,30 @@ __global__ void __launch_bounds__(kKsThreads) kskip_kernel(KskipArgs a) {
       acc3_mac(su, x0, x1, lo30(ya), hi30(ya));
       acc3_mac(sv, x0, x1, lo30(yb), hi30(yb));
     }
-    uo[o] = acc3_reduce(su, P);
-    vo[o] = acc3_reduce(sv, P);
+    uo[o] = a.accumulate ? addmod(uo[o], acc3_reduce(su, P), P.q) : acc3_reduce(su, P);
+    vo[o] = a.accumulate ? addmod(vo[o], acc3_reduce(sv, P), P.q) : acc3_reduce(sv, P);
   }
 }
 
-int launch_kskip(const KskipArgs& a, int rows, int batch, cudaStream_t st) {
+int launch_kskip(const KskipArgs& a0, int rows, int batch, cudaStream_t st) {
   if (rows <= 0 || batch <= 0) return 0;
-  if (a.beta < 1 || a.beta > kKsMaxBeta) return CK_ERR_ARG;
+  if (a0.beta < 1) return CK_ERR_ARG;
+  if (a0.beta > kKsMaxBeta) {
+    // any dnum: chunks of kKsMaxBeta digits, later chunks accumulate into u, v
+    for (int d0 = 0; d0 < a0.beta; d0 += kKsMaxBeta) {
+      KskipArgs c = a0;
+      c.beta = a0.beta - d0 < kKsMaxBeta ? a0.beta - d0 : kKsMaxBeta;
+      c.digits = a0.digits + d0 * a0.digit_stride;
+      if (c.key_b) c.key_b += d0 * a0.key_digit_stride;
+      if (c.key_a) c.key_a += d0 * a0.key_digit_stride;
+      c.key_digit0 = a0.key_digit0 + d0;
+      c.accumulate = a0.accumulate || d0 > 0;
+      const int e = launch_kskip(c, rows, batch, st);
+      if (e) return e;
+    }
+    return 0;
+  }
+  const KskipArgs& a = a0;
   const int n = 1 << a.logn;
   count_launches(1);
   if (n >= 512) {

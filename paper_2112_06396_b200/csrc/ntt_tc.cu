@@ -364,217 +364,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// Ping-pong form: 2 warpgroups x 8 warps, each owning TWO accumulator slots
-// (2 x 128 TMEM columns) and two tiles in flight, so every epilogue overlaps
-// the other slot's MMA instead of waiting for its own:
-//   ... epi2(a) -> MMA1(a') | epi2(b) -> MMA1(b') | epi1(a') -> MMA2(a') |
-//       epi1(b') -> MMA2(b') | epi2(a') -> ...
-// Per slot two A buffers: the next tile streams in (cp.async) while the
-// current one is on the tensor cores.  One (possibly empty) cp.async group is
-// committed per prefetch, so "wait_group 1" always means "my tile has landed".
-constexpr int kPpWG = 2;                      // warpgroups per CTA
-constexpr int kPpThreads = 32 * kTcGW * kPpWG;
-
-template <int P2, bool INV>
-__global__ void __launch_bounds__(kPpThreads, 1) ntt_col_tc2_kernel(NttArgs a) {
-  extern __shared__ __align__(1024) unsigned char tsm[];
-  // A[wg][slot][buf] (16 KB each), then B1 | B2, twists, mbarriers [wg][slot]
-  unsigned char* Bm = tsm + kPpWG * 4 * kOpBytes;
-  ulonglong2* tw = (ulonglong2*)(Bm + 2 * kBBytes);
-  uint64_t* mbar = (uint64_t*)(tw + 256);
-  uint32_t* tslot = (uint32_t*)(mbar + 2 * kPpWG);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wg = warp / kTcGW, gw = warp % kTcGW, gtid = tid % (32 * kTcGW);
-  const int quarter = gw & 3, half = gw >> 2;
-  const int job = blockIdx.y;
-  const int prime = a.prime_idx[job];
-  const u64 p = a.pc[prime].q;
-  const u32 m81 = tc_m81(p);
-  u64* base = a.data + (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) +
-              (long long)blockIdx.z * a.batch_stride;
-  const unsigned mb0 = (unsigned)__cvta_generic_to_shared(mbar + 2 * wg);
-  const unsigned mb1 = mb0 + 8;
-  const unsigned abuf_s = (unsigned)__cvta_generic_to_shared(tsm) + wg * 4 * kOpBytes;
-  unsigned char* abuf = tsm + wg * 4 * kOpBytes;
-  const unsigned b_s = (unsigned)__cvta_generic_to_shared(Bm);
-  const int cbase = blockIdx.x * kTcTiles * kTcCols;
-  const int bar_id = 1 + wg;
-  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kTcGW) : "memory"); };
-  // this WG's tiles: wg, wg + 2, ...; slot s takes every other one
-  constexpr int NT = kTcTiles / kPpWG;
-  auto tile_c0 = [&](int i) { return cbase + (wg + kPpWG * i) * kTcCols; };
-  auto a_s = [&](int slot, int buf) { return abuf_s + (slot * 2 + buf) * kOpBytes; };
-  auto a_g = [&](int slot, int buf) { return abuf + (slot * 2 + buf) * kOpBytes; };
-
-  pdl_trigger();
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-        (unsigned)__cvta_generic_to_shared(tslot)), "n"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (gtid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb1));
-  }
-  {
-    const uint4* src = (const uint4*)(a.tcB + ((size_t)prime * 4 + (INV ? 2 : 0)) * kBBytes);
-    uint4* dst = (uint4*)Bm;
-    for (int i = tid; i < 2 * kBBytes / 16; i += kPpThreads) dst[i] = __ldg(src + i);
-    const ulonglong2* ts = a.tcD + ((size_t)prime * 2 + (INV ? 1 : 0)) * 256;
-    for (int i = tid; i < 256; i += kPpThreads) tw[i] = __ldg(ts + i);
-  }
-  pdl_wait();  // the predecessor's output is read from here on
-  // prologue loads: tile 0 -> slot 0, tile 1 -> slot 1 (one group each)
-  stage_tile<P2, INV>(a_s(0, 0), base, tile_c0(0), gw, lane);
-  stage_tile<P2, INV>(a_s(1, 0), base, tile_c0(1), gw, lane);
-  const ulonglong2 scl = !INV ? make_ulonglong2(0, 0)
-                              : (a.scale ? a.scale[job] : make_ulonglong2(a.pc[prime].ninv, a.pc[prime].ninvp));
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = *tslot + wg * 256;
-  const int m = quarter * 32 + lane;  // this thread's D row
-  unsigned ph0 = 0, ph1 = 0;
-
-  auto mma = [&](int slot, unsigned a_addr, unsigned b_addr) {
-    if (gtid == 0) {
-      const uint32_t tacc = tbase + slot * 128;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) mma_i8(tacc, smem_desc(a_addr + s * 256), smem_desc(b_addr + s * 256), s > 0);
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          slot ? mb1 : mb0) : "memory");
-    }
-  };
-  // my slot's tile has landed (cp.async), is visible to the tensor core, and the
-  // slot's previous TMEM reads are complete: issue MMA1
-  auto start_pass1 = [&](int slot, int buf) {
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    fence_async_smem();
-    tc_fence_before();
-    gsync();
-    tc_fence_after();
-    mma(slot, a_s(slot, buf), b_s);
-  };
-  auto wait_slot = [&](int slot) {
-    if (slot) { mbar_wait(mb1, ph1); ph1 ^= 1; }
-    else { mbar_wait(mb0, ph0); ph0 ^= 1; }
-    tc_fence_after();
-  };
-  auto epi1 = [&](int slot, int buf) {
-    unsigned char* A = a_g(slot, buf);
-    const uint32_t tl = tbase + slot * 128 + ((uint32_t)(quarter * 32) << 16);
-    const int g1 = m >> 3, c = m & 7;
-#pragma unroll 1
-    for (int h = 2 * half; h < 2 * half + 2; ++h) {   // 4 outputs (32 TMEM columns) per wait
-      uint32_t sv[32];
-      tmem_ld32(tl + h * 32, sv);
-      tmem_wait_ld();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int o = h * 4 + u;                      // pass-1 output index
-        const u64 y = reduce_lazy(sv + 8 * u, p, m81);
-        const ulonglong2 d = tw[o * 16 + g1];
-        st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, p));  // [0, 4p)
-      }
-    }
-    fence_async_smem();
-    tc_fence_before();
-    gsync();
-    tc_fence_after();
-    mma(slot, a_s(slot, buf), b_s + kBBytes);
-  };
-  auto epi2 = [&](int slot, int i) {
-    const uint32_t tl = tbase + slot * 128 + ((uint32_t)(quarter * 32) << 16);
-    const int o1 = m >> 3, c = m & 7;
-    u64* col = base + tile_c0(i) + c;
-#pragma unroll 1
-    for (int h = 2 * half; h < 2 * half + 2; ++h) {
-      uint32_t sv[32];
-      tmem_ld32(tl + h * 32, sv);
-      tmem_wait_ld();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int o2 = h * 4 + u;
-        const u64 v = reduce_lazy(sv + 8 * u, p, m81);
-        if (INV)  // rows 16 o2 + o1; canonical (the base conversion needs exact residues)
-          col[(long long)(o2 * 16 + o1) << P2] = csub(csub(shoup_tc(v, scl.x, scl.y, p), 2 * p), p);
-        else      // rows 16 o1 + o2; lazy (0, 4p)
-          col[(long long)(o2 + 16 * o1) << P2] = v;
-      }
-    }
-  };
-  auto prefetch = [&](int slot, int buf, int i) {   // always one commit group
-    if (i < NT) stage_tile<P2, INV>(a_s(slot, buf), base, tile_c0(i), gw, lane);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  // prologue MMAs + the next pair's loads
-  start_pass1(0, 0);
-  prefetch(0, 1, 2);
-  start_pass1(1, 0);
-  prefetch(1, 1, 3);
-#pragma unroll 1
-  for (int pr = 0; 2 * pr < NT; ++pr) {
-    const int buf = pr & 1, i0 = 2 * pr, i1 = 2 * pr + 1;
-    wait_slot(0);
-    epi1(0, buf);           // -> MMA2 on slot 0 (overlaps slot 1's MMA1)
-    wait_slot(1);
-    epi1(1, buf);           // -> MMA2 on slot 1
-    wait_slot(0);
-    epi2(0, i0);            // overlaps slot 1's MMA2
-    if (i0 + 2 < NT) {
-      start_pass1(0, buf ^ 1);       // next tile of slot 0 (loaded during this pair)
-      prefetch(0, buf, i0 + 4);      // buf is free again: its MMA2 completed
-    }
-    wait_slot(1);
-    epi2(1, i1);            // overlaps slot 0's next MMA1
-    if (i1 + 2 < NT) {
-      start_pass1(1, buf ^ 1);
-      prefetch(1, buf, i1 + 4);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(512));
-  }
-}
-
-constexpr size_t kPpSmem = kPpWG * 4 * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 64;
-
 constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 64;
 
 template <int P2, bool INV>
-int launch_pp(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
-  static unsigned done = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 32 || !((done >> dev) & 1u)) {
-    cudaFuncSetAttribute(ntt_col_tc2_kernel<P2, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kPpSmem);
-    if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);
-  }
-  const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
-  launch_pdl(ntt_col_tc2_kernel<P2, INV>, grid, dim3(kPpThreads), kPpSmem, st, a);
-  return 0;
-}
-
-static bool use_pp() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CKB200_TCPP");
-    v = e ? (e[0] == '1') : 1;
-  }
-  return v == 1;
-}
-
-template <int P2, bool INV>
 int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
-  if (use_pp()) return launch_pp<P2, INV>(a, jobs, batch, st);
   // the shared-memory opt-in is per device: track it per device ordinal
   static unsigned done = 0;  // bit d: set on device d (ordinals < 32)
   int dev = 0;

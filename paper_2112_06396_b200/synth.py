@@ -3,7 +3,7 @@
 BASELINE.json's inputs are "residues uniform in [0, q_i) from seed".  Full
 configs are too large to draw on the host (C3: 8 GB of keys, C5: 110 GB),
 so inputs come from a counter-based generator that the CUDA library
-(``ck_fill_uniform``, csrc/synth.cu) evaluates bit-identically:
+(``ck_fill_uniform``, csrc/ew.cu ``fill_uniform_kernel``) evaluates bit-identically:
 
     key(seed, stream) = splitmix64(splitmix64(seed) ^ stream)
     x_k               = splitmix64(key + k)

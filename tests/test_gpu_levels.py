@@ -166,3 +166,33 @@ def test_hoisted_paths_fused_ring_match_oracle(kind):
         got = [x for pair in gb.hrotate(p, a, b, keys, rots) for x in pair]
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
+
+
+def test_many_digits_beyond_fused_limit():
+    """dnum = 12 (beta = 12 > 8 digits): the KSKIP runs in digit chunks that
+    accumulate; rotation, hoisted rotations and relinearisation stay bit-exact
+    against the oracle (the reference has no dnum cap, ckks.py:31-65)."""
+    p = _params(12, 12, 1, 12, cb=50, sb=51)
+    assert len(p.digit_spans(p.limbs)) == 12
+    a, b, kb, ka = synth.rotation_inputs(p, 5, 0)
+    want = ckks_np.rotate_galois(p, a, b, kb, ka, pow(5, 3, 2 * p.n_ring))
+    ks = ckks.KeySet(p, None, None, rot={-3: ckks.SwitchingKey(p.full_moduli, kb, a=ka)})
+
+    def ct(x, y):
+        return ckks.Ciphertext(RnsPoly(p.chain, to_dev(x), "eval"), RnsPoly(p.chain, to_dev(y), "eval"),
+                               p.delta)
+
+    c1 = ct(a, b)
+    got = ckks.rotate(p, ks, c1, -3)
+    assert np.array_equal(to_host(got.a.data), want[0])
+    assert np.array_equal(to_host(got.b.data), want[1])
+    gh = ckks.hrotate(p, ks, c1, (-3,))[0]
+    assert np.array_equal(to_host(gh.a.data), want[0])
+    assert np.array_equal(to_host(gh.b.data), want[1])
+    a2 = synth.uniform_poly(5, 1, synth.TAG_CT2_A, p.chain, p.n_ring)
+    b2 = synth.uniform_poly(5, 1, synth.TAG_CT2_B, p.chain, p.n_ring)
+    rk = synth.switching_key(p, 5, 998)
+    wa, wb = ckks_np.new_mult(p, (a, b), (a2, b2), rk)
+    ksr = ckks.KeySet(p, None, ckks.SwitchingKey(p.full_moduli, rk[0], a=rk[1]))
+    o = ckks.new_mult(p, ksr, c1, ct(a2, b2))
+    assert np.array_equal(to_host(o.a.data), wa) and np.array_equal(to_host(o.b.data), wb)
