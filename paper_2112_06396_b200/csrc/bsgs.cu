@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(diag_threads<MB>(), 4) diag_mac_kernel(DiagArg
     __syncthreads();
   }
   if (c >= n) return;
-  const PrimeConst& P = a.pc[a.prime[i]];
+  const PrimeConst P = a.pc[a.prime[i]];  // a register copy: global reads of P would reload after every store
   const long long rowN = (long long)a.R << a.logn;
   const long long off = ((long long)i << a.logn) + c;
   const int nk = (a.baby + KL - 1) / KL;   // chunks per giant group
@@ -159,6 +159,170 @@ int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
   else if (a.baby <= 16) CK_DIAG(16);
   else CK_DIAG(32);
 #undef CK_DIAG
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Fused baby-step KSKIP + diagonal MAC.  One thread = one coefficient c of one
+// raised row i.  Per baby k (compile-time unrolled, MB <= 16): its BETA digit
+// values at the automorphism's source index and its 2 BETA key words arrive by
+// per-thread 8-byte cp.async (a ring NSB babies deep, thread-private columns:
+// no barriers); u_k = sum_d digit_d[perm_k(c)] key_a[k][d][i][c],
+// v_k = sum_d digit_d[perm_k(c)] key_b[k][d][i][c] + [P] b[i][perm_k(c)] stay in
+// registers (_kskip + pmodup, ckks.py:450-465, 478-489, 699-711).  Then per
+// giant group j the MB diagonals of row i stream in (ring NSG giants deep) and
+//   acc_u[j] = sum_k diag[j][k] u_k,  acc_v[j] = sum_k diag[j][k] v_k.
+constexpr int kBmNT = 128, kBmNSB = 3, kBmNSG = 2, kBmMB = 16;
+template <int BETA>
+constexpr size_t bsgs_mac_smem() {
+  return (size_t)(kBmNSB * 3 * BETA + kBmNSG * kBmMB) * kBmNT * 8 + (2 * kBmMB + 512) * 8;
+}
+
+template <int BETA>
+__global__ void __launch_bounds__(kBmNT, 2) bsgs_mac_kernel(BsgsMacArgs a) {
+  constexpr int NT = kBmNT, MB = kBmMB, NSB = kBmNSB, NSG = kBmNSG;
+  extern __shared__ __align__(16) u64 bsm[];
+  u64 (*bs)[3 * BETA][NT] = (u64 (*)[3 * BETA][NT])bsm;                       // [NSB][3 BETA][NT]
+  u64 (*gs)[MB][NT] = (u64 (*)[MB][NT])(bsm + NSB * 3 * BETA * NT);          // [NSG][MB][NT]
+  const u64** kbp = (const u64**)(bsm + (NSB * 3 * BETA + NSG * MB) * NT);   // [MB]
+  const u64** kap = kbp + MB;                                                 // [MB]
+  const u64** dps = kap + MB;                                                 // [giant][baby]
+  const DiagArgs& d = a.d;
+  const int n = 1 << d.logn;
+  const int c = blockIdx.x * NT + threadIdx.x;
+  const int i = blockIdx.y;
+  const int t = threadIdx.x;
+  const int baby = d.baby, giant = d.giant;
+  for (int e = t; e < baby; e += NT) {
+    kbp[e] = a.key_b_ptrs[e];
+    kap[e] = a.key_a_ptrs[e];
+  }
+  for (int e = t; e < giant * baby; e += NT)
+    dps[e] = d.diag_ptrs[(long long)(e / baby) * d.diag_stride + e % baby];
+  __syncthreads();
+  if (c >= n) return;
+  const int prime = d.prime[i];
+  const PrimeConst P = d.pc[prime];
+  const long long rowN = (long long)d.R << d.logn;
+  const long long off = ((long long)i << d.logn) + c;
+  const long long koff = ((long long)prime << d.logn) + c;  // key row i == prime index
+  const bool chain = i < d.l;
+  // baby k's operands -> ring slot k % NSB (one commit group per baby, possibly empty)
+  auto stage_baby = [&](int k) {
+    if (k < baby) {
+      const int s = k % NSB;
+      const u32 src = automorph_src((u32)c, (u32)d.galois[k], d.logn);
+      const u64* dg = a.digits + ((long long)i << d.logn) + src;
+#pragma unroll
+      for (int dd = 0; dd < BETA; ++dd) {
+        cp_async8(&bs[s][dd][t], dg + dd * a.digit_stride);
+        cp_async8(&bs[s][BETA + dd][t], kap[k] + dd * a.key_digit_stride + koff);
+        cp_async8(&bs[s][2 * BETA + dd][t], kbp[k] + dd * a.key_digit_stride + koff);
+      }
+    }
+    cp_async_commit();
+  };
+  auto stage_giant = [&](int j) {
+    if (j < giant) {
+      const int s = j % NSG;
+#pragma unroll
+      for (int k = 0; k < MB; ++k)
+        if (k < baby) cp_async8(&gs[s][k][t], dps[j * baby + k] + off);
+    }
+    cp_async_commit();
+  };
+  const ulonglong2 pm = chain ? d.pmod[i] : make_ulonglong2(0, 0);
+  u64 x[2 * MB];
+#pragma unroll
+  for (int k = 0; k < NSB - 1; ++k) stage_baby(k);
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    stage_baby(k + NSB - 1);
+    cp_async_wait<NSB - 1>();
+    if (k < baby) {
+      const int s = k % NSB;
+      Acc3 su, sv;
+      acc3_zero(su);
+      acc3_zero(sv);
+#pragma unroll
+      for (int dd = 0; dd < BETA; ++dd) {
+        const u64 dv = bs[s][dd][t], ka = bs[s][BETA + dd][t], kb = bs[s][2 * BETA + dd][t];
+        const u32 d0 = lo30(dv), d1 = hi30(dv);
+        acc3_mac(su, d0, d1, lo30(ka), hi30(ka));
+        acc3_mac(sv, d0, d1, lo30(kb), hi30(kb));
+      }
+      x[2 * k] = acc3_reduce(su, P);
+      u64 v = acc3_reduce(sv, P);
+      if (chain) {
+        const u64 bv = d.b[((long long)i << d.logn) +
+                           automorph_src((u32)c, (u32)d.galois[k], d.logn)];
+        v = addmod(v, shoup(bv, pm.x, pm.y, P.q), P.q);
+      }
+      x[2 * k + 1] = v;
+    }
+  }
+  // drain the (empty) baby groups, then stream the giant groups' diagonals
+  cp_async_wait<0>();
+#pragma unroll
+  for (int j = 0; j < NSG - 1; ++j) stage_giant(j);
+#pragma unroll 1
+  for (int j = 0; j < giant; ++j) {
+    stage_giant(j + NSG - 1);
+    cp_async_wait<NSG - 1>();
+    const int s = j % NSG;
+    u64 yu = d.accumulate ? d.acc[(2LL * j) * rowN + off] : 0;
+    u64 yv = d.accumulate ? d.acc[(2LL * j + 1) * rowN + off] : 0;
+#pragma unroll
+    for (int k0 = 0; k0 < MB; k0 += 8) {
+      if (k0 >= baby) continue;
+      Acc3 su, sv;
+      acc3_zero(su);
+      acc3_zero(sv);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = k0 + kk;
+        if (k < baby) {
+          const u64 mv = gs[s][k][t];
+          const u32 m0 = lo30(mv), m1 = hi30(mv);
+          acc3_mac(su, m0, m1, lo30(x[2 * k]), hi30(x[2 * k]));
+          acc3_mac(sv, m0, m1, lo30(x[2 * k + 1]), hi30(x[2 * k + 1]));
+        }
+      }
+      yu = addmod(yu, acc3_reduce(su, P), P.q);
+      yv = addmod(yv, acc3_reduce(sv, P), P.q);
+    }
+    d.acc[(2LL * j) * rowN + off] = yu;
+    d.acc[(2LL * j + 1) * rowN + off] = yv;
+  }
+}
+
+int launch_bsgs_mac(const BsgsMacArgs& a, cudaStream_t st) {
+  const DiagArgs& d = a.d;
+  if (d.baby < 1 || d.baby > kBmMB || d.giant < 1 || d.giant * d.baby > 512 || a.beta < 1 ||
+      a.beta > 4 || !d.diag_ptrs || !a.key_b_ptrs || !a.key_a_ptrs || d.logn < 7)
+    return -1;
+  count_launches(1);
+  const int n = 1 << d.logn;
+  const dim3 grid((n + kBmNT - 1) / kBmNT, d.R);
+#define CK_BM(B)                                                                            \
+  do {                                                                                      \
+    static unsigned done = 0;                                                               \
+    int dev = 0;                                                                            \
+    cudaGetDevice(&dev);                                                                    \
+    if (dev >= 32 || !((done >> dev) & 1u)) {                                               \
+      cudaFuncSetAttribute(bsgs_mac_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)bsgs_mac_smem<B>());                                        \
+      if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);                  \
+    }                                                                                       \
+    bsgs_mac_kernel<B><<<grid, kBmNT, bsgs_mac_smem<B>(), st>>>(a);                        \
+  } while (0)
+  switch (a.beta) {
+    case 1: CK_BM(1); break;
+    case 2: CK_BM(2); break;
+    case 3: CK_BM(3); break;
+    default: CK_BM(4); break;
+  }
+#undef CK_BM
   return (int)cudaGetLastError();
 }
 

@@ -212,6 +212,7 @@ struct ck_plan {
   int logn = 0, n = 0, L = 0, K = 0, dnum = 0, alpha = 0, key_digits = 0;
   bool fused = true;  // CKB200_UNFUSED=1 at plan creation selects the unfused pipeline
   int md_group = 4;   // md_row items per CTA (CKB200_MD_G)
+  int bsgs_fused = 1; // fused baby KSKIP + diagonal MAC (CKB200_BSGS_FUSED=0: two kernels)
   int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
   int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
@@ -847,6 +848,7 @@ int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t
     const char* e = getenv("CKB200_UNFUSED");
     p->fused = !(e && e[0] == '1');
     if (const char* mg = getenv("CKB200_MD_G")) p->md_group = std::max(1, atoi(mg));
+    if (const char* bf = getenv("CKB200_BSGS_FUSED")) p->bsgs_fused = atoi(bf);
     const char* tc = getenv("CKB200_BCTC");
     if (tc) p->bc_tc = atoi(tc);
   }
@@ -1330,11 +1332,8 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
   CK_TRY(modup_impl(p, level, a, dig, tmp, 1, st));
   for (int c0 = 0; c0 < baby; c0 += chunk) {
     const int cnt = std::min(chunk, baby - c0);
-    // 2. the chunk's baby KSKIPs in one launch: digits shared, per-baby key and Galois element
-    CK_TRY(kskip_impl(p, level, dig, keys_ptrs(bkeys.bp, bkeys.ap, c0), 1, bgal + c0, uvb,
-                      uvb + R * N, 2 * R * N, cnt, st, true));
-    // 3. diagonal MAC into giant accumulators (pmodup(automorph(b)) folded in);
-    //    chunks after the first accumulate
+    // 2+3. baby KSKIPs and the diagonal MAC into the giant accumulators
+    //      (pmodup(automorph(b)) folded in); chunks after the first accumulate
     ck::DiagArgs da{};
     da.uv = uvb;
     da.b = b;
@@ -1351,7 +1350,22 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
     da.R = (int)R;
     da.l = level;
     da.logn = p->logn;
-    CK_TRY(ck::launch_diag_mac(da, st));
+    // fused: baby outputs stay in registers (no u_k / v_k round trip through HBM)
+    ck::BsgsMacArgs ba;
+    ba.d = da;
+    ba.digits = dig;
+    ba.digit_stride = R * N;
+    ba.key_b_ptrs = bkeys.bp + c0;
+    ba.key_a_ptrs = bkeys.ap + c0;
+    ba.key_digit_stride = (long long)(p->L + p->K) * N;
+    ba.beta = t.beta;
+    const int e = p->bsgs_fused ? ck::launch_bsgs_mac(ba, st) : -1;
+    if (e > 0) return e;
+    if (e < 0) {
+      CK_TRY(kskip_impl(p, level, dig, keys_ptrs(bkeys.bp, bkeys.ap, c0), 1, bgal + c0, uvb,
+                        uvb + R * N, 2 * R * N, cnt, st, true));
+      CK_TRY(ck::launch_diag_mac(da, st));
+    }
   }
   // 4. merged ModDown (P * q_last) of every accumulator -> level l-1
   if (ck::fused_supported(p->logn) && p->fused) {

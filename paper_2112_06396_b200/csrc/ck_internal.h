@@ -147,6 +147,21 @@ struct DiagArgs {
 };
 int launch_diag_mac(const DiagArgs& a, cudaStream_t st);
 
+// Fused hoisted baby-step KSKIP + diagonal MAC (bsgs.cu bsgs_mac_kernel): the
+// baby outputs (u_k, v_k + P automorph(b, t_k)) stay in registers and feed the
+// giant accumulators directly -- they never touch HBM.
+struct BsgsMacArgs {
+  DiagArgs d;                   // uv unused; galois = baby Galois elements
+  const u64* digits;            // [beta][R][N] shared ModUp digits (evaluation form)
+  long long digit_stride;       // R N
+  const u64* const* key_b_ptrs; // [baby] per-baby key blocks [dnum][L+K][N]
+  const u64* const* key_a_ptrs;
+  long long key_digit_stride;   // (L+K) N
+  int beta;
+};
+// returns -1 when the shape is not covered (the caller runs kskip + diag_mac)
+int launch_bsgs_mac(const BsgsMacArgs& a, cudaStream_t st);
+
 // Basis conversion: ns source rows (coefficient rep, same coefficient index)
 // -> nd destination rows.  T[i*nd+j] = (Q/q_i) mod p_j.
 struct BconvArgs {

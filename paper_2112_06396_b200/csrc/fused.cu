@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   const int i = blockIdx.z + a.row0;   // grid (row tile, batch, limb): twiddle reuse across the batch
   const long long b = blockIdx.y;
   const int prime = a.prime[i];
-  const PrimeConst& P = a.pc[prime];
-  const u64 q = P.q, two_q = P.two_q;
+  const PrimeConst& Pg = a.pc[prime];
+  const u64 q = Pg.q, two_q = Pg.two_q;
   const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
   const int r = blockIdx.x * F::TR + rl;
   const u64 t = a.galois ? a.galois[b] : a.galois_t;
@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   // CTA's contiguous TR*S tile, so key loads / u,v stores are 16-byte
   // vectors and every warp instruction covers 512 contiguous bytes.
   // Output column c of row r reads column pi_r(c) of row sigma(r).
+  // reduction constants in registers for the MAC loop only (loaded after the
+  // NTTs: a reference into global memory would reload them after every store)
+  const PrimeConst P = Pg;
   const long long tile0 = (long long)blockIdx.x * F::TR << P2;
   const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
   const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   __shared__ u64 stage[F::TR * F::RS];
   const int j = blockIdx.z;  // grid (row tile, item group, limb)
   const int prime = a.prime[j];
-  const PrimeConst& P = a.pc[prime];
+  const PrimeConst& P = a.pc[prime];  // (a register copy spills at 64 registers)
   const u64 q = P.q, two_q = P.two_q;
   const ulonglong2 pinv = a.pinv[j];
   const int rl = threadIdx.x / F::G, g = threadIdx.x % F::G;
