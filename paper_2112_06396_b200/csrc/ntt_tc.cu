@@ -73,9 +73,6 @@ __device__ __forceinline__ uint64_t smem_desc(unsigned saddr) {
 constexpr uint32_t kIdesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
-#ifdef CKB200_ABL_MMA
-  return;
-#endif
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
@@ -116,9 +113,6 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // One mul.hi replaces the FP64 estimate (whose DADD/DFMA bursts throttled the
 // FP64 pipe in every epilogue); the byte-plane assembly stays on the ALU pipe.
 __device__ __forceinline__ u64 reduce_lazy(const uint32_t* s, u64 p, u32 m81) {
-#ifdef CKB200_ABL_RED
-  return ((u64)s[1] << 32) | s[0];
-#endif
   const u32 P0 = s[0] + (s[1] << 8), P1 = s[2] + (s[3] << 8);
   const u32 P2 = s[4] + (s[5] << 8), P3 = s[6] + (s[7] << 8);
   u32 lo, hi, ml, mh;
@@ -169,9 +163,6 @@ __device__ __forceinline__ u32 tc_m81(u64 p) {
 // The next tensor-core pass accepts any 64-bit operand; canonical outputs
 // fold it with two conditional subtractions.
 __device__ __forceinline__ u64 shoup_tc(u64 x, u64 w, u64 wp, u64 p) {
-#ifdef CKB200_ABL_TWIST
-  return x;
-#endif
   const u32 xl = (u32)x, xh = (u32)(x >> 32);
   const u32 wl = (u32)w, wh = (u32)(w >> 32);
   const u32 wpl = (u32)wp, wph = (u32)(wp >> 32);
