@@ -279,6 +279,9 @@ template <int P1, int P2, bool LAZY>
 #ifndef CKB200_MD_MINB
 #define CKB200_MD_MINB 8
 #endif
+#ifndef CKB200_MD_CALL
+#define CKB200_MD_CALL 1
+#endif
 __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
@@ -305,6 +308,19 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   const long long b = a.pair ? (item >> 1) : item;
   const u64* conv = a.conv + b * a.conv_batch + ro + (a.pair && w ? a.conv_w : 0);
   const u64* x = a.x + b * a.x_batch + ro + (a.pair && w ? a.x_w : 0);
+#if CKB200_MD_CALL
+  // the row NTT as the shared non-inlined ks_digit_ntt (smaller kernel code:
+  // md_row's fully inlined form is ~54 KB of SASS, above the instruction cache)
+  {
+    u64 y[kE];
+#pragma unroll
+    for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
+    row_to_smem<P2, 0, false>(y, g, srow);
+  }
+  ks_digit_ntt<P2, LOGN>(srow, g, r, tw, q, two_q);  // lazy [0,16q); q >= 2^56 canonical
+  constexpr bool lazy = LAZY;
+  __syncthreads();
+#else
   u64 y[kE];
 #pragma unroll
   for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
@@ -319,6 +335,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   __syncthreads();
   row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, srow);
   __syncthreads();
+#endif
   u64 o[kE];
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
