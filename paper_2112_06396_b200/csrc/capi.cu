@@ -831,7 +831,7 @@ const char* ck_error_string(int code) {
 
 int ck_plan_create(int log_n, const uint64_t* chain, int n_chain, const uint64_t* special,
                    int n_special, int dnum, ck_plan** out) {
-  if (!out || log_n < 1 || log_n > 17 || n_chain < 1 || n_special < 0 || dnum < 1 || !chain ||
+  if (!out || log_n < 1 || log_n > 20 || n_chain < 1 || n_special < 0 || dnum < 1 || !chain ||
       (n_special > 0 && !special))
     return CK_ERR_ARG;
   int ndev = 0;

@@ -413,7 +413,7 @@ static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t
   return 0;
 }
 
-bool fused_supported(int logn) { return logn >= 12 && logn <= 17; }
+bool fused_supported(int logn) { return logn >= 12 && logn <= 20; }
 
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
   if (rows <= 0 || batch <= 0) return 0;
@@ -426,6 +426,9 @@ int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
     case 15: launch_ks_row_t<7, 8>(a, rows, batch, st); break;
     case 16: launch_ks_row_t<8, 8>(a, rows, batch, st); break;
     case 17: launch_ks_row_t<8, 9>(a, rows, batch, st); break;
+    case 18: launch_ks_row_t<9, 9>(a, rows, batch, st); break;
+    case 19: launch_ks_row_t<9, 10>(a, rows, batch, st); break;
+    case 20: launch_ks_row_t<10, 10>(a, rows, batch, st); break;
     default: return CK_ERR_ARG;
   }
   return (int)cudaGetLastError();
@@ -441,6 +444,9 @@ int launch_md_row(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
     case 15: launch_md_row_t<7, 8>(a, rows, batch, st); break;
     case 16: launch_md_row_t<8, 8>(a, rows, batch, st); break;
     case 17: launch_md_row_t<8, 9>(a, rows, batch, st); break;
+    case 18: launch_md_row_t<9, 9>(a, rows, batch, st); break;
+    case 19: launch_md_row_t<9, 10>(a, rows, batch, st); break;
+    case 20: launch_md_row_t<10, 10>(a, rows, batch, st); break;
     default: return CK_ERR_ARG;
   }
   return (int)cudaGetLastError();

@@ -15,11 +15,12 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 #define CKB200_NTT_MINB 3
 #endif
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(kTC * (1 << P1) / kE, CKB200_NTT_MINB)
+__global__ void __launch_bounds__(col_tc<P1>() * (1 << P1) / kE, CKB200_NTT_MINB)
 ntt_col_kernel(NttArgs a) {
   constexpr int S = 1 << P1;
+  constexpr int TC = col_tc<P1>();
   constexpr int NP = Sched<P1>::np;
-  __shared__ u64 sm[S * kTC];
+  __shared__ u64 sm[S * TC];
   __shared__ ulonglong2 tws[S];
   const int job = blockIdx.y;
   const int prime = a.prime_idx[job];
@@ -29,8 +30,8 @@ ntt_col_kernel(NttArgs a) {
     for (int i = threadIdx.x; i < S; i += blockDim.x) tws[i] = tw[i];
   }
   u64* base = a.data + job_offset(a, job, blockIdx.z);
-  const int col = threadIdx.x % kTC, g = threadIdx.x / kTC;
-  const int c = blockIdx.x * kTC + col;
+  const int col = threadIdx.x % TC, g = threadIdx.x / TC;
+  const int c = blockIdx.x * TC + col;
   u64 x[kE];
 #pragma unroll
   for (int r = 0; r < kE; ++r) x[r] = base[((long long)sub_index<P1, 0, INV>(g, r) << P2) + c];
@@ -39,20 +40,20 @@ ntt_col_kernel(NttArgs a) {
   CK_COL_PASS(0)
   if constexpr (NP > 1) {
 #pragma unroll
-    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 0, INV>(g, r) * kTC + col] = x[r];
+    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 0, INV>(g, r) * TC + col] = x[r];
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 1, INV>(g, r) * kTC + col];
+    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 1, INV>(g, r) * TC + col];
     if (!INV) fwd_fold(x, q << 3);
     CK_COL_PASS(1)
   }
   if constexpr (NP > 2) {
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 1, INV>(g, r) * kTC + col] = x[r];
+    for (int r = 0; r < kE; ++r) sm[sub_index<P1, 1, INV>(g, r) * TC + col] = x[r];
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 2, INV>(g, r) * kTC + col];
+    for (int r = 0; r < kE; ++r) x[r] = sm[sub_index<P1, 2, INV>(g, r) * TC + col];
     if (!INV) fwd_fold(x, q << 3);
     CK_COL_PASS(2)
   }
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(512) ntt_small_kernel(NttArgs a) {
 template <int P1, int P2>
 static void launch_split(const NttArgs& a, int jobs, int batch, bool inv, int phase,
                          cudaStream_t st) {
-  const dim3 gcol((1 << P2) / kTC, jobs, batch), bcol(kTC * (1 << P1) / kE);
+  const dim3 gcol((1 << P2) / col_tc<P1>(), jobs, batch), bcol(col_tc<P1>() * (1 << P1) / kE);
   using R = RowCfg<P2>;
   const dim3 grow((1 << P1) / R::TR, batch, jobs), brow(R::TR * R::G);
   const bool col = phase != 2, row = phase != 1;
@@ -237,6 +238,9 @@ int launch_ntt_phase(const NttArgs& a, int jobs, int batch, bool inverse, int ph
     case 15: launch_split<7, 8>(a, jobs, batch, inverse, phase, st); break;
     case 16: launch_split<8, 8>(a, jobs, batch, inverse, phase, st); break;
     case 17: launch_split<8, 9>(a, jobs, batch, inverse, phase, st); break;
+    case 18: launch_split<9, 9>(a, jobs, batch, inverse, phase, st); break;
+    case 19: launch_split<9, 10>(a, jobs, batch, inverse, phase, st); break;
+    case 20: launch_split<10, 10>(a, jobs, batch, inverse, phase, st); break;
     default: {
       if (phase != 0 || a.logn < 1 || a.logn > 11) return CK_ERR_ARG;
       count_launches(1);

@@ -25,6 +25,10 @@ namespace ck {
 constexpr int kElog = 4;
 constexpr int kE = 1 << kElog;  // elements per thread
 constexpr int kTC = 16;         // columns per column-phase CTA (128 B rows)
+// columns per column-phase CTA for a 2^P1-row column: 16 up to 256 rows, fewer
+// above so the CTA's shared tile (2^P1 x TC words) stays within 32 KB
+template <int P1>
+CK_HD constexpr int col_tc() { return P1 <= 8 ? kTC : (P1 == 9 ? 8 : 4); }
 
 struct NttArgs {
   u64* data;

@@ -196,3 +196,29 @@ def test_many_digits_beyond_fused_limit():
     ksr = ckks.KeySet(p, None, ckks.SwitchingKey(p.full_moduli, rk[0], a=rk[1]))
     o = ckks.new_mult(p, ksr, c1, ct(a2, b2))
     assert np.array_equal(to_host(o.a.data), wa) and np.array_equal(to_host(o.b.data), wb)
+
+
+@pytest.mark.parametrize("logn", [18, 19, 20])
+def test_large_rings_ntt_match_oracle(logn):
+    """N = 2^18 .. 2^20 (column/row splits 512x512 .. 1024x1024): forward NTT of one limb
+    bit-exact against the oracle, and INTT(NTT(x)) == x on two limbs."""
+    from paper_2112_06396_b200.rnspoly import ntt_rows
+    chain, _ = prime_chain_below(1 << logn, 54, 2, 60, 0)
+    x = synth.uniform_poly(9, 0, synth.TAG_NTT, chain, 1 << logn)
+    f = ntt_rows(to_dev(x), tuple(chain), False)
+    assert np.array_equal(to_host(f[:1]), ckks_np.ntt(x[:1], chain[:1]))
+    assert np.array_equal(to_host(ntt_rows(f, tuple(chain), True)), x)
+
+
+def test_large_ring_rotation_matches_oracle():
+    """A fused rotation key-switch at N = 2^18 (the reference has no ring-size cap)."""
+    p = _params(18, 3, 1, 3, cb=54, sb=60)
+    a, b, kb, ka = synth.rotation_inputs(p, 5, 0)
+    t = pow(5, 7, 2 * p.n_ring)
+    want = ckks_np.rotate_galois(p, a, b, kb, ka, t)
+    ks = ckks.KeySet(p, None, None, rot={-7: ckks.SwitchingKey(p.full_moduli, kb, a=ka)})
+    ct = ckks.Ciphertext(RnsPoly(p.chain, to_dev(a), "eval"), RnsPoly(p.chain, to_dev(b), "eval"),
+                         p.delta)
+    got = ckks.rotate(p, ks, ct, -7)
+    assert np.array_equal(to_host(got.a.data), want[0])
+    assert np.array_equal(to_host(got.b.data), want[1])
