@@ -172,14 +172,26 @@ int launch_diag_mac(const DiagArgs& a, cudaStream_t st) {
 // registers (_kskip + pmodup, ckks.py:450-465, 478-489, 699-711).  Then per
 // giant group j the MB diagonals of row i stream in (ring NSG giants deep) and
 //   acc_u[j] = sum_k diag[j][k] u_k,  acc_v[j] = sum_k diag[j][k] v_k.
-constexpr int kBmNT = 128, kBmNSB = 3, kBmNSG = 2, kBmMB = 16;
+#ifndef CKB200_BM_NSB
+#define CKB200_BM_NSB 2
+#endif
+#ifndef CKB200_BM_NSG
+#define CKB200_BM_NSG 2
+#endif
+#ifndef CKB200_BM_NT
+#define CKB200_BM_NT 128
+#endif
+constexpr int kBmNT = CKB200_BM_NT, kBmNSB = CKB200_BM_NSB, kBmNSG = CKB200_BM_NSG, kBmMB = 16;
 template <int BETA>
 constexpr size_t bsgs_mac_smem() {
   return (size_t)(kBmNSB * 3 * BETA + kBmNSG * kBmMB) * kBmNT * 8 + (2 * kBmMB + 512) * 8;
 }
 
 template <int BETA>
-__global__ void __launch_bounds__(kBmNT, 2) bsgs_mac_kernel(BsgsMacArgs a) {
+#ifndef CKB200_BM_MINB
+#define CKB200_BM_MINB 2
+#endif
+__global__ void __launch_bounds__(kBmNT, CKB200_BM_MINB) bsgs_mac_kernel(BsgsMacArgs a) {
   constexpr int NT = kBmNT, MB = kBmMB, NSB = kBmNSB, NSG = kBmNSG;
   extern __shared__ __align__(16) u64 bsm[];
   u64 (*bs)[3 * BETA][NT] = (u64 (*)[3 * BETA][NT])bsm;                       // [NSB][3 BETA][NT]

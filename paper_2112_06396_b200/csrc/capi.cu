@@ -594,12 +594,28 @@ int modup_impl(const ck_plan* p, int l, const u64* a, u64* digits, u64* tmp, int
   const LevelTab& t = p->lv[l];
   const long long N = p->n;
   const long long dig_b = (long long)t.beta * t.R * N;
-  CK_TRY((int)cudaMemcpyAsync(tmp, a, sizeof(u64) * B * l * N, cudaMemcpyDeviceToDevice, st));
   // INTT of every chain row, scaled by its digit's ihat (rnspoly.py:274-275)
-  CK_TRY(ntt_rows(p, tmp, t.d_chain_prime, nullptr, t.d_modup_scale, l, B, l * N, true, st));
-  for (int d = 0; d < t.beta; ++d)
-    CK_TRY(bconv_run(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
-                     false, B, st));
+  if (ck::fused_supported(p->logn)) {
+    // row phase reads the input directly (no copy), then the column phase
+    CK_TRY(ntt_phase(p, tmp, t.d_chain_prime, nullptr, nullptr, l, B, l * N, true, 2, st, a,
+                     l * N));
+    CK_TRY(ntt_phase(p, tmp, t.d_chain_prime, nullptr, t.d_modup_scale, l, B, l * N, true, 1,
+                     st));
+  } else {
+    CK_TRY((int)cudaMemcpyAsync(tmp, a, sizeof(u64) * B * l * N, cudaMemcpyDeviceToDevice, st));
+    CK_TRY(ntt_rows(p, tmp, t.d_chain_prime, nullptr, t.d_modup_scale, l, B, l * N, true, st));
+  }
+  if (t.beta <= ck::kMaxBcGroups) {  // all digits' conversions in one launch
+    ck::BconvArgs gs[ck::kMaxBcGroups];
+    for (int d = 0; d < t.beta; ++d)
+      gs[d] = bconv_args(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
+                         false);
+    CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
+  } else {
+    for (int d = 0; d < t.beta; ++d)
+      CK_TRY(bconv_run(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
+                       false, B, st));
+  }
   CK_TRY(ntt_rows(p, digits, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
                   dig_b, false, st));
   for (int d = 0; d < t.beta; ++d) {
