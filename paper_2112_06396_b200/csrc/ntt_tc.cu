@@ -79,6 +79,9 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
 }
 
+__device__ __forceinline__ unsigned mbar_addr(const uint64_t* b) {
+  return (unsigned)__cvta_generic_to_shared(b);
+}
 __device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
@@ -227,8 +230,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   unsigned char* Bm = tsm + 2 * kTcGroups * kOpBytes;      // A[group][2] (16 KB each), then B1 | B2
   ulonglong2* tw = (ulonglong2*)(Bm + 2 * kBBytes);        // twists [beta][r_lo] (4 KB)
-  uint64_t* mbar = (uint64_t*)(tw + 256);                  // [group]
-  uint32_t* tslot = (uint32_t*)(mbar + kTcGroups);
+  uint64_t* mbar = (uint64_t*)(tw + 256);                  // [group], then the table barrier
+  uint64_t* tbar = mbar + kTcGroups;
+  uint32_t* tslot = (uint32_t*)(tbar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = warp / kTcGW, gw = warp % kTcGW, gtid = tid % (32 * kTcGW);
@@ -254,12 +258,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (gtid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s));
-  {
-    const uint4* src = (const uint4*)(a.tcB + ((size_t)prime * 4 + (INV ? 2 : 0)) * kBBytes);
-    uint4* dst = (uint4*)Bm;
-    for (int i = tid; i < 2 * kBBytes / 16; i += kTcThreads) dst[i] = __ldg(src + i);
-    const ulonglong2* ts = a.tcD + ((size_t)prime * 2 + (INV ? 1 : 0)) * 256;
-    for (int i = tid; i < 256; i += kTcThreads) tw[i] = __ldg(ts + i);
+  if (tid == 0) {
+    // the prime's B1 | B2 matrices (32 KB) and twists (4 KB): two TMA bulk copies,
+    // in flight while the predecessor drains (plan tables, not its output)
+    mbar_init(tbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(tbar, 2 * kBBytes + 256 * sizeof(ulonglong2));
+    bulk_g2s(Bm, a.tcB + ((size_t)prime * 4 + (INV ? 2 : 0)) * kBBytes, 2 * kBBytes, tbar);
+    bulk_g2s(tw, a.tcD + ((size_t)prime * 2 + (INV ? 1 : 0)) * 256, 256 * sizeof(ulonglong2), tbar);
   }
   pdl_wait();  // the predecessor's output is read from here on
   stage_tile<P2, INV>(abuf_s, base, cbase + grp * kTcCols, gw, lane);  // this group's first tile
@@ -269,6 +275,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  mbar_wait(mbar_addr(tbar), 0);  // B matrices and twists have landed
   const uint32_t tacc = *tslot + grp * 128;                     // this group's accumulator columns
   const uint32_t tl = tacc + ((uint32_t)(quarter * 32) << 16);  // this warp's lane quarter
   const int m = quarter * 32 + lane;                            // this thread's D row
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   }
 }
 
-constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 64;
+constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 72;
 
 template <int P2, bool INV>
 int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
