@@ -178,14 +178,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-// exact double of a 32-bit integer on the FP64 pipe: bits(0x43300000:v) - 2^52
-__device__ __forceinline__ double u32_to_f64(u32 v) {
-  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);
-}
-
 struct TcTarget {
   u64 p;
-  double pinv;
+  u32 m;        // floor(2^(sh+32) / p)
+  int sh;       // floor(log2 p)
   long long off;
 };
 
@@ -236,7 +232,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kern
   for (int i = tid; i < tks * ntile * 32; i += blockDim.x) bf[i] = a.Bf[i];
   for (int j = tid; j < nd; j += blockDim.x) {
     const u64 p = a.pc[a.dst_prime[j]].q;
-    tg[j] = TcTarget{p, 1.0 / (double)p, a.out_off ? a.out_off[j] : ((long long)j << a.logn)};
+    const int sh = 63 - __clzll((long long)p);
+    const u32 m = (u32)(((unsigned __int128)1 << (sh + 32)) / p);
+    tg[j] = TcTarget{p, m, sh, a.out_off ? a.out_off[j] : ((long long)j << a.logn)};
   }
   if (a.centered)
     for (int i = tid; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
@@ -319,14 +317,15 @@ __global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kern
             const u32 P1 = (u32)acc[mb][1][2 * h] + ((u32)acc[mb][1][2 * h + 1] << 8);
             const u32 P2 = (u32)acc[mb][2][2 * h] + ((u32)acc[mb][2][2 * h + 1] << 8);
             const u32 P3 = (u32)acc[mb][3][2 * h] + ((u32)acc[mb][3][2 * h + 1] << 8);
-            // V mod 2^64 and round(V / p) (P0 / p < 2^-18 is dropped from the estimate)
+            // V mod 2^64, and an integer quotient: W = floor(V / 2^sh) < 2^32 (V/p < 2^31,
+            // checked at plan time), qh = floor(W m / 2^32) undershoots V/p by less than 3
+            // (dropped low bits of V: < 2^sh/p <= 1; m's floor; qh's floor), so
+            // V - qh p is in [0, 3p): two conditional subtractions give the canonical residue
             const u64 vlo = (u64)P0 + ((u64)P1 << 16) + ((u64)P2 << 32) + ((u64)P3 << 48);
-            const double vd = __fma_rn(u32_to_f64(P3), 281474976710656.0,
-                                       __fma_rn(u32_to_f64(P2), 4294967296.0,
-                                                __dmul_rn(u32_to_f64(P1), 65536.0)));
-            const u32 qh = (u32)__double2loint(__fma_rn(vd, T.pinv, 6755399441055744.0));
-            u64 r = vlo - (u64)qh * T.p;           // in (-p, p) as a signed value
-            r += ((long long)r < 0) ? T.p : 0ull;
+            const u64 vhi = ((u64)P3 << 16) + P2 + (P1 >> 16);  // floor(V / 2^32), to within 1
+            const u32 qh = __umulhi((u32)(vhi >> (T.sh - 32)), T.m);
+            u64 r = vlo - (u64)qh * T.p;
+            r = csub(csub(r, 2 * T.p), T.p);
             const int row = warp * 32 + mb * 16 + h * 8 + gid;
             if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[row]], T.p);
             if (row0 + row < n) out[T.off + row0 + row] = r;

@@ -340,13 +340,16 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
       c3248[2 * j] = sh2(((u64)1 << 32) % pj, pj);
       c3248[2 * j + 1] = sh2(((u64)1 << 48) % pj, pj);
     }
-    // The FP64 quotient of the epilogue must fit 31 bits: bound V = sum_b S_b 2^8b
+    // The epilogue quotient V/p must fit 31 bits: bound V = sum_b S_b 2^8b
     // with S_b <= 32 ks 255^2 (every k-step byte, padding included) and check
     // V / p_j + 1 < 2^31 for every target (C3: p > 2^53; C5's 50-bit chain: 2^28.6).
     const double s_max = 32.0 * ks * 255.0 * 255.0;
     const double v_max = s_max * 257.0 * (1.0 + 65536.0 + 4294967296.0 + 281474976710656.0);
     bool big = true;
-    for (int j = 0; j < nd; ++j) big = big && v_max / (double)p->mod[dst[j]] + 2.0 < 2147483648.0;
+    // (the epilogue's integer quotient also shifts by floor(log2 p) - 32 >= 0)
+    for (int j = 0; j < nd; ++j)
+      big = big && v_max / (double)p->mod[dst[j]] + 2.0 < 2147483648.0 &&
+            p->mod[dst[j]] > ((u64)1 << 40);
     b->tc_ks = big ? ks : 0;
     b->d_Bf = upload(b->allocs, Bf, err);
     b->d_c3248 = upload(b->allocs, c3248, err);
