@@ -64,7 +64,7 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const 
     for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
   }
   __syncthreads();
-  row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+  row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
 }
 
 // ---------------------------------------------------------------- KSKIP row
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
 #pragma unroll
       for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
       __syncthreads();
-      row_to_smem<P2, Sched<P2>::np - 1, false>(x, g, srow);
+      row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
     }
   }
   }
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
     for (int k = 0; k < kE; ++k) y[k] = fwd_final(y[k], q);
   }
   __syncthreads();
-  row_to_smem<P2, Sched<P2>::np - 1, false>(y, g, srow);
+  row_to_smem<P2, RowLast<P2>::value, false>(y, g, srow);
   __syncthreads();
 #endif
   u64 o[kE];

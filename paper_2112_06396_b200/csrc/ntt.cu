@@ -129,7 +129,9 @@ ntt_row_kernel(NttArgs a) {
     if (!INV) fwd_fold(x, q << 3);
     run_pass<P2, 1, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
   }
-  if constexpr (NP > 2) {
+  if constexpr (P2 == 9) {
+    last_level_shfl<P2, INV, P1 + P2>(x, g, jbase, tw, q, two_q);
+  } else if constexpr (NP > 2) {
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, 1, INV>(g, r))] = x[r];
@@ -147,14 +149,14 @@ ntt_row_kernel(NttArgs a) {
     for (int r = 0; r < kE; ++r) x[r] = fwd_final(x[r], q);
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, NP - 1, INV>(g, r))] = x[r];
+    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, RowLast<P2>::value, INV>(g, r))] = x[r];
     __syncthreads();
     u64* tile = base + ((long long)blockIdx.x * R::TR << P2);
     for (int i = threadIdx.x; i < R::TR * R::S; i += blockDim.x)
       tile[i] = sm[(i >> P2) * R::RS + sidx(i & (R::S - 1))];
   } else {
 #pragma unroll
-    for (int r = 0; r < kE; ++r) rowp[sub_index<P2, NP - 1, INV>(g, r)] = x[r];
+    for (int r = 0; r < kE; ++r) rowp[sub_index<P2, RowLast<P2>::value, INV>(g, r)] = x[r];
   }
 }
 

@@ -166,6 +166,56 @@ CK_D void bar_arrive_n(int id, int nt) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nt) : "memory");
 }
 
+// The lone 9th level of a 512-point row (P = 9: passes of 4 + 4 + 1 levels) without
+// a third shared-memory round trip: in the pass-1 layout a row is one warp and the
+// level's partner elements sit in lane g^1 (forward, distance 1) or g^16 (inverse,
+// distance 256) at the SAME register index.  The lower lane computes the pairs of
+// registers k < 8, the upper lane those of k >= 8 (8 butterflies each, no
+// divergence): one shuffle brings each lane the other operand, one more returns
+// the partner's result.  Values stay in the pass-1 layout (RowLast<9> = 1).
+CK_D u64 shfl_xor64(u64 v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+template <int P, bool INV, int LOGN>
+CK_D void last_level_shfl(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict__ tw,
+                          u64 q, u64 two_q) {
+  static_assert(P == 9 && kE == 16, "512-point rows: 32 threads = one warp per row");
+  constexpr int X = INV ? 16 : 1;  // lane distance of the partner
+  const bool lower = (g & X) == 0;  // holds the pairs' first (lower-index) elements
+  if (!INV) fwd_fold(x, q << 3);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const u64 recv = shfl_xor64(lower ? x[kk + 8] : x[kk], X);
+    const int k = lower ? kk : kk + 8;
+    u64 xv = lower ? x[kk] : recv;        // first element of pair k
+    u64 yv = lower ? recv : x[kk + 8];    // second element of pair k
+    const int j = jbase + sub_index<P, 1, INV>(g & ~X, k);
+    if (!INV) {
+      const ulonglong2 w = __ldg(tw + (1 << (LOGN - 1)) + (j >> 1));
+      const u64 t = shoup_tw(yv, w.x, w.y, q, two_q);
+      const u64 xx = xv;
+      xv = xx + t;
+      yv = xx - t + two_q;
+    } else {
+      const ulonglong2 w = __ldg(tw + (1 << (LOGN - 9)) + (j >> 9));
+      bfly_gs(xv, yv, w.x, w.y, q, two_q);
+    }
+    const u64 back = shfl_xor64(lower ? yv : xv, X);
+    if (lower) {
+      x[kk] = xv;
+      x[kk + 8] = back;
+    } else {
+      x[kk + 8] = yv;
+      x[kk] = back;
+    }
+  }
+}
+
+// Pass whose layout holds a row's final values (row_to_smem after row_transform).
+template <int P>
+struct RowLast {
+  static constexpr int value = P == 9 ? 1 : Sched<P>::np - 1;
+};
+
 template <int P2, bool INV, int LOGN, class Sync = SyncCta>
 CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
                         const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
@@ -181,90 +231,15 @@ CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
     if (!INV) fwd_fold(x, q << 3);
     run_pass<P2, 1, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
   }
-  if constexpr (NP > 2) {
+  if constexpr (P2 == 9) {
+    last_level_shfl<P2, INV, LOGN>(x, g, jbase, tw, q, two_q);
+  } else if constexpr (NP > 2) {
     Sync::sync();
     row_to_smem<P2, 1, INV>(x, g, srow);
     Sync::sync();
     row_from_smem<P2, 2, INV>(x, g, srow);
     if (!INV) fwd_fold(x, q << 3);
     run_pass<P2, 2, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
-  }
-}
-
-// Row-phase pass with the CTA's row twiddles staged in shared memory.
-// Layout (tw_row_stage): stage s of the row phase (2^s twiddles per row)
-// occupies TR * 2^s entries at offset TR * (2^s - 1), row-major by local row.
-template <int P, int p, bool INV, int LOGN, int TR>
-CK_D void run_pass_rs(u64 (&x)[kE], int g, int rl, const ulonglong2* __restrict__ tws, u64 q,
-                      u64 two_q) {
-  constexpr int C = Sched<P>::C(p);
-  constexpr int LD = Sched<P>::logD(p, INV);
-  constexpr int NG = kE >> C;
-#pragma unroll
-  for (int h = 0; h < NG; ++h) {
-    const int s0 = sub_index<P, p, INV>(g, h << C);
-#pragma unroll
-    for (int st = 0; st < C; ++st) {
-      const int lhalf = INV ? st : (C - 1 - st);
-      const int half = 1 << lhalf;
-      const int logt = LD + lhalf;            // within-row distance
-      const int s = P - 1 - logt;             // row-phase stage: 2^s twiddles per row
-#pragma unroll
-      for (int b = 0; b < (1 << C) / (2 * half); ++b) {
-        const int k0 = b * 2 * half;
-        const int c = s0 + (k0 << LD);
-        const ulonglong2 w = tws[TR * ((1 << s) - 1) + (rl << s) + (c >> (logt + 1))];
-#pragma unroll
-        for (int k = k0; k < k0 + half; ++k) {
-          u64& X = x[(h << C) + k];
-          u64& Y = x[(h << C) + k + half];
-          if (INV) {
-            bfly_gs(X, Y, w.x, w.y, q, two_q);
-          } else {
-            const u64 t = shoup_tw(Y, w.x, w.y, q, two_q);
-            const u64 xx = X;
-            X = xx + t;
-            Y = xx - t + two_q;
-          }
-        }
-      }
-    }
-  }
-}
-
-// Stage the twiddles of rows [r0, r0+TR) of a 2^P-point row phase.
-template <int P, int P1, int TR, int NT>
-CK_D void tw_row_stage(ulonglong2* tws, const ulonglong2* __restrict__ tw, int r0) {
-#pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const ulonglong2* src = tw + (1 << (P1 + s)) + ((long long)r0 << s);
-    for (int i = threadIdx.x; i < (TR << s); i += NT) tws[TR * ((1 << s) - 1) + i] = __ldg(src + i);
-  }
-}
-
-// Full row phase with staged twiddles (see row_transform).
-template <int P2, bool INV, int LOGN, int TR>
-CK_D void row_transform_rs(u64 (&x)[kE], int g, int rl, u64* srow, const ulonglong2* tws, u64 q,
-                           u64 two_q) {
-  constexpr int NP = Sched<P2>::np;
-  static_assert(NP <= 3, "row too long");
-  if (!INV) fwd_fold(x, q << 3);
-  run_pass_rs<P2, 0, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
-  if constexpr (NP > 1) {
-    __syncthreads();
-    row_to_smem<P2, 0, INV>(x, g, srow);
-    __syncthreads();
-    row_from_smem<P2, 1, INV>(x, g, srow);
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass_rs<P2, 1, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
-  }
-  if constexpr (NP > 2) {
-    __syncthreads();
-    row_to_smem<P2, 1, INV>(x, g, srow);
-    __syncthreads();
-    row_from_smem<P2, 2, INV>(x, g, srow);
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass_rs<P2, 2, INV, LOGN, TR>(x, g, rl, tws, q, two_q);
   }
 }
 
