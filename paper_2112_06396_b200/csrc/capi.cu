@@ -1336,7 +1336,8 @@ int ck_bsgs(const ck_plan* p, const uint64_t* a_, const uint64_t* b_,
   const LevelTab& t = p->lv[level];
   const ModDownTab& m = t.md[1];
   const long long N = p->n, l = level, R = t.R, lo = l - 1;
-  const int chunk = std::min(baby, kDiagChunk);
+  // chunks of 16 babies for the fused kernel (its register-resident baby outputs), 32 else
+  const int chunk = std::min(baby, p->bsgs_fused ? 16 : kDiagChunk);
   u64* dig = ws;
   u64* tmp = dig + (long long)t.beta * R * N;
   u64* uvb = tmp + l * N;                        // [chunk][2][R][N]

@@ -222,3 +222,30 @@ def test_large_ring_rotation_matches_oracle():
     got = ckks.rotate(p, ks, ct, -7)
     assert np.array_equal(to_host(got.a.data), want[0])
     assert np.array_equal(to_host(got.b.data), want[1])
+
+
+@pytest.mark.parametrize("kind,count", [("bsgs", 20), ("bsgs", 33), ("pt_matvec", 33), ("pt_matvec", 65)])
+def test_chunk_boundaries_fused_ring(kind, count):
+    """Chunked accumulation across launches at N = 2^12: BSGS with 20 / 33 babies (fused
+    kernel in chunks of 16), pt_matvec with 33 / 65 diagonals (chunks of 32)."""
+    p = _params(12, 4, 2, 2)
+    mods, raised = p.chain, p.raised_moduli(p.limbs)
+    a = cases._rows(p, 0, synth.TAG_CT_A, mods)
+    b = cases._rows(p, 0, synth.TAG_CT_B, mods)
+    ob, gb = cases.OracleBackend(), gpu_backend.GpuBackend()
+    if kind == "bsgs":
+        baby, giant = count, 2
+        diags = {(j, k): cases._rows(p, j, synth.TAG_DIAG, raised, digit=k)
+                 for j in range(1, giant + 1) for k in range(1, baby + 1)}
+        rs = sorted({-k for k in range(1, baby + 1)} | {-baby * j for j in range(1, giant + 1)})
+        keys = cases._keys(p, rs)
+        want = ob.bsgs(p, a, b, keys, diags, baby, giant)
+        got = gb.bsgs(p, a, b, keys, diags, baby, giant)
+    else:
+        offs = tuple(range(-(count // 2), count - count // 2))
+        assert len(offs) == count and 0 in offs
+        diags = {o: cases._rows(p, 0, synth.TAG_DIAG, raised, digit=o % 64) for o in offs}
+        keys = cases._keys(p, [-o for o in offs if o % p.slots])
+        want, got = ob.pt_matvec(p, a, b, keys, diags), gb.pt_matvec(p, a, b, keys, diags)
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
