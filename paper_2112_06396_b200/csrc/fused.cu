@@ -32,12 +32,20 @@ struct FusedCfg {
   static constexpr int RS = row_stride<P2>();
 };
 #ifndef CKB200_KS_EPC
-#define CKB200_KS_EPC 2048
+#define CKB200_KS_EPC 1024
 #endif
 #ifndef CKB200_KS_MINB
-#define CKB200_KS_MINB 4
+#define CKB200_KS_MINB 5
 #endif
-constexpr int kKsEpc = CKB200_KS_EPC;  // ks_row elements per CTA (2048: 128 threads, 4 CTAs/SM)
+// CKB200_KS_RING = S > 0: the key tiles reach shared memory through a ring of S
+// stages of TMA bulk copies (one stage = one MAC iteration's 2*BETA key segments),
+// the first S issued at kernel start so they land during the digit NTTs
+#ifndef CKB200_KS_RING
+#define CKB200_KS_RING 2
+#endif
+// ks_row elements per CTA (1024: 64 threads; with the 2-stage key ring 38 KB of SMEM, 5 CTAs/SM;
+// measured against 2048 elements x 4 CTAs, rings of 1-8 stages and 2-5 CTAs/SM: DESIGN section 10)
+constexpr int kKsEpc = CKB200_KS_EPC;
 
 // Forward row phase of one digit tile in shared memory (natural order in and
 // out).  Not inlined (CKB200_KS_NOINLINE, default 1): ONE copy of this code per kernel instead
@@ -95,12 +103,40 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   const ulonglong2* tw = a.tw + ((long long)prime << LOGN);
   constexpr int NB = BETA > 0 ? BETA : 8;
   const int beta = BETA > 0 ? BETA : a.beta;
+  constexpr int NSK = BETA > 0 ? CKB200_KS_RING : 0;
+  constexpr int SEG = 2 * F::NT;                          // words per key segment (one iteration)
+  u64* ring = fsm + (BETA > 0 ? BETA : 0) * SLOT;         // [NSK][2 BETA][SEG]
+  uint64_t* kbar = (uint64_t*)(ring + NSK * 2 * (BETA > 0 ? BETA : 1) * SEG);
+  const long long ktile0 = (long long)blockIdx.x * F::TR << P2;
+  const u64* kta = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + ktile0;
+  const u64* ktb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + ktile0;
+  auto ring_issue = [&](int m) {  // thread 0: iteration m's 2 BETA segments into slot m % NSK
+    if constexpr (NSK > 0) {
+      const int sl = m % NSK;
+      mbar_expect_tx(&kbar[sl], (unsigned)(2 * BETA * SEG * 8));
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        bulk_g2s(ring + (sl * 2 * BETA + 2 * d) * SEG, kta + d * a.key_digit_stride + SEG * m,
+                 SEG * 8, &kbar[sl]);
+        bulk_g2s(ring + (sl * 2 * BETA + 2 * d + 1) * SEG, ktb + d * a.key_digit_stride + SEG * m,
+                 SEG * 8, &kbar[sl]);
+      }
+    }
+  };
+  if constexpr (NSK > 0) {
+    constexpr int ITER0 = (F::TR * F::S) / (2 * F::NT);
+    if (threadIdx.x == 0) {
+      for (int sl = 0; sl < NSK; ++sl) mbar_init(&kbar[sl], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int m = 0; m < NSK && m < ITER0; ++m) ring_issue(m);  // keys are inputs: before the PDL wait
+    }
+  }
 
   // Key tiles are only needed after the digit NTTs: start streaming them to L2
   // now (one bulk prefetch per key row-tile, contiguous TR*S words), so the
   // inner product below hits L2 instead of waiting on HBM.
   // key_prefetch = k: prefetch the first k/8 of each key row-tile (k = 8: all)
-  if (a.key_prefetch && threadIdx.x < 2 * beta) {
+  if (NSK == 0 && a.key_prefetch && threadIdx.x < 2 * beta) {
     const int d = threadIdx.x >> 1;
     const u64* kbase = (threadIdx.x & 1) ? key_block(a.key_a, a.key_a_ptrs, a.key_batch, b)
                                          : key_block(a.key_b, a.key_b_ptrs, a.key_batch, b);
@@ -176,10 +212,52 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
   const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
   u64* ubase = a.uv + b * a.uv_batch + ((long long)i << LOGN);
-  u64* uo = ubase + ((long long)r << P2);
-  u64* vo = uo + a.v_off;
   constexpr int ITER = (F::TR * F::S) / (2 * F::NT);
-  if constexpr (BETA > 0) {
+  if constexpr (BETA > 0 && NSK > 0) {
+    // keys from the TMA ring: iteration m waits for its stage, frees it after a barrier
+#pragma unroll 1
+    for (int m = 0; m < ITER; ++m) {
+      const int e = 2 * (int)threadIdx.x + 2 * F::NT * m;
+      const int sl = m % NSK;
+      mbar_wait_parity(&kbar[sl], (unsigned)((m / NSK) & 1));
+      ulonglong2 ya[BETA], yb[BETA];
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        ya[d] = *(const ulonglong2*)(ring + (sl * 2 * BETA + 2 * d) * SEG + 2 * threadIdx.x);
+        yb[d] = *(const ulonglong2*)(ring + (sl * 2 * BETA + 2 * d + 1) * SEG + 2 * threadIdx.x);
+      }
+      const int er = e >> P2, ec = e & (F::S - 1);
+      const int rr = blockIdx.x * F::TR + er;
+      int sc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        sc[h] = t == 1 ? ec + h
+                       : (int)(automorph_src(((u32)rr << P2) + ec + h, (u32)t, LOGN) & (F::S - 1));
+      Acc3 su[2], sv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc3_zero(su[h]);
+        acc3_zero(sv[h]);
+      }
+#pragma unroll
+      for (int d = 0; d < BETA; ++d) {
+        const u64* drow = fsm + d * SLOT + er * F::RS;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const u64 x = drow[sidx(sc[h])];
+          const u64 ax = h ? ya[d].y : ya[d].x, bx = h ? yb[d].y : yb[d].x;
+          const u32 x0 = lo30(x), x1 = hi30(x);
+          acc3_mac(su[h], x0, x1, lo30(ax), hi30(ax));
+          acc3_mac(sv[h], x0, x1, lo30(bx), hi30(bx));
+        }
+      }
+      u64* uw = ubase + tile0 + e;
+      *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
+      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+      __syncthreads();  // every thread is done with slot sl
+      if (threadIdx.x == 0 && m + NSK < ITER) ring_issue(m + NSK);
+    }
+  } else if constexpr (BETA > 0) {
     // software-pipelined: the key vectors of iteration m+1 are in flight while
     // iteration m multiplies (the MAC phase is otherwise load-latency bound)
     ulonglong2 ya[BETA], yb[BETA];
@@ -377,8 +455,12 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
 template <int P1, int P2>
 static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t st) {
   using F = FusedCfg<P2, kKsEpc>;
-  const size_t smem = (size_t)a.beta * F::TR * F::RS * 8;
   const int bsel = a.beta <= 4 ? a.beta : 0;
+  // digit slots (+ the key ring and its mbarriers for compile-time BETA)
+  const size_t ring = bsel && CKB200_KS_RING
+                          ? (size_t)CKB200_KS_RING * (2 * bsel * 2 * F::NT * 8 + 8)
+                          : 0;
+  const size_t smem = (size_t)a.beta * F::TR * F::RS * 8 + ring;
   auto kern = bsel == 1   ? ks_row_kernel<P1, P2, 1>
               : bsel == 2 ? ks_row_kernel<P1, P2, 2>
               : bsel == 3 ? ks_row_kernel<P1, P2, 3>
@@ -392,7 +474,7 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
     const unsigned bit = dev < 32 ? 1u << dev : 0u;
     if (!bit || !(done[bsel].load(std::memory_order_relaxed) & bit)) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((size_t)(bsel ? bsel : 8) * F::TR * F::RS * 8));
+                           (int)((size_t)(bsel ? bsel : 8) * F::TR * F::RS * 8 + ring));
       done[bsel].fetch_or(bit, std::memory_order_relaxed);
     }
   }
