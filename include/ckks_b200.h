@@ -122,6 +122,17 @@ int ck_rotate(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const u
               int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
               ck_stream stream);
 
+/* ---- one entry for every key-switch flavour (SURVEY 8(b) ck_keyswitch) ----
+ * mode 0: rotation (ck_rotate mode 0), 1: conjugation (ck_rotate mode 1), one
+ * key per batch item as ck_rotate takes them ([batch][dnum][L+K][N]);
+ * 2: relinearisation (ck_relin): `a` = a3 [batch][level][N] and `b` = (b3, c3) as
+ * [batch][2][level][N]; outputs [batch][level-1][N]; galois_t / galois ignored, the
+ * key is one relin key shared by the batch.  Workspace: ck_keyswitch_workspace_bytes. */
+size_t ck_keyswitch_workspace_bytes(const ck_plan* plan, int level, int mode, int batch);
+int ck_keyswitch(const ck_plan* plan, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
+                 const uint64_t* key_a, int level, uint64_t galois_t, const uint64_t* galois,
+                 int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
+                 ck_stream stream);
 /* ---- relinearisation key-switch of new_mult (ckks.py:639-651) ----
  * (a3, b3, c3) at `level` chain limbs (value_mult / addend / const already
  * folded into b3, c3 by the caller, ckks.py:624-638) ->

@@ -39,6 +39,9 @@ _SIGS = [
     ("ck_moddown", C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp, C.c_uint64, vp, C.c_int, vp]),
     ("ck_rotate", C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_uint64, vp, C.c_int, vp, vp, vp,
                             C.c_int, vp]),
+    ("ck_keyswitch_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int, C.c_int]),
+    ("ck_keyswitch", C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_uint64, vp, C.c_int, vp, vp, vp,
+                               C.c_int, vp]),
     ("ck_relin_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),
     ("ck_relin", C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, vp]),
     ("ck_hrotate_workspace_bytes", C.c_size_t, [vp, C.c_int, C.c_int]),

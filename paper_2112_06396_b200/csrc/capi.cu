@@ -753,6 +753,7 @@ int moddown_pairs(const ck_plan* p, const ModDownTab& m, u64* x, long long R, u6
 struct Relin {
   const u64* b3;
   const u64* c3;
+  long long stride;  // elements between batch items of b3 (and of c3)
 };
 int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_add,
                     const Keys& keys, u64 kgt, const u64* kgal, u64 egt, const u64* egal,
@@ -817,14 +818,15 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
     const int* lp = t.d_chain_prime + (l - 1);
     const ulonglong2* pm = t.d_pmod + (l - 1);
     CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + (l - 1) * N, 2 * R * N, w.uv + (l - 1) * N, 2 * R * N,
-                  relin->b3 + (l - 1) * N, l * N, nullptr, 0, lp, pm, 1, nullptr, 1, B, st));
+                  relin->b3 + (l - 1) * N, relin->stride, nullptr, 0, lp, pm, 1, nullptr, 1, B, st));
     CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + (R + l - 1) * N, 2 * R * N, w.uv + (R + l - 1) * N,
-                  2 * R * N, relin->c3 + (l - 1) * N, l * N, nullptr, 0, lp, pm, 1, nullptr, 1, B,
+                  2 * R * N, relin->c3 + (l - 1) * N, relin->stride, nullptr, 0, lp, pm, 1, nullptr, 1, B,
                   st));
   }
   // ---- ModDown pair (fused): INTT, BC, column phase, md_row epilogue
   return moddown_pairs(p, m, w.uv, R, w.conv, B, out_a, out_b, relin ? relin->c3 : b_add,
-                       relin ? relin->b3 : nullptr, relin ? m.d_dinv : nullptr, l * N,
+                       relin ? relin->b3 : nullptr, relin ? m.d_dinv : nullptr,
+                       relin ? relin->stride : l * N,
                        relin ? 1 : egt, relin ? nullptr : egal, st);
 }
 
@@ -1127,6 +1129,13 @@ int rotate_impl(const ck_plan* p, const u64* a, const u64* b, const Keys& keys, 
 }
 }  // namespace
 
+namespace {
+int relin_impl(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const uint64_t* c3_,
+               long long bc_stride, const uint64_t* key_b, const uint64_t* key_a, int level,
+               uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, int batch,
+               ck_stream stream);
+}  // namespace
+
 extern "C" {
 
 int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const uint64_t* key_b_,
@@ -1139,14 +1148,38 @@ int ck_rotate(const ck_plan* p, const uint64_t* a_, const uint64_t* b_, const ui
                      batch, (cudaStream_t)stream);
 }
 
+size_t ck_keyswitch_workspace_bytes(const ck_plan* p, int level, int mode, int batch) {
+  if (mode < 0 || mode > 2 || batch < 1) return 0;
+  return mode == 2 ? ck_relin_workspace_bytes(p, level, batch) : ck_workspace_bytes(p, level, batch);
+}
+
+int ck_keyswitch(const ck_plan* p, const uint64_t* a, const uint64_t* b, const uint64_t* key_b,
+                 const uint64_t* key_a, int level, uint64_t galois_t, const uint64_t* galois,
+                 int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* workspace, int batch,
+                 ck_stream stream) {
+  if (mode == 0 || mode == 1)
+    return ck_rotate(p, a, b, key_b, key_a, level, galois_t, galois, mode, out_a, out_b,
+                     workspace, batch, stream);
+  if (mode != 2 || !p || !b) return CK_ERR_ARG;
+  const long long ln = (long long)level * p->n;
+  return relin_impl(p, a, b, b + ln, 2 * ln, key_b, key_a, level, out_a, out_b, workspace, batch,
+                    stream);
+}
+
 size_t ck_relin_workspace_bytes(const ck_plan* p, int level, int batch) {
   if (!level_ok(p, level) || level < 2 || batch < 1) return 0;
   return ck_workspace_bytes(p, level, batch);
 }
 
-int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const uint64_t* c3_,
-             const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a_,
-             uint64_t* out_b_, uint64_t* workspace_, int batch, ck_stream stream) {
+}  // extern "C"
+
+namespace {
+// bc_stride: elements between batch items of b3 and of c3 (level N for ck_relin,
+// 2 level N for ck_keyswitch's interleaved (b3, c3) block)
+int relin_impl(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const uint64_t* c3_,
+               long long bc_stride, const uint64_t* key_b, const uint64_t* key_a, int level,
+               uint64_t* out_a_, uint64_t* out_b_, uint64_t* workspace_, int batch,
+               ck_stream stream) {
   const u64 *a3 = (const u64*)a3_, *b3 = (const u64*)b3_, *c3 = (const u64*)c3_;
   u64 *out_a = (u64*)out_a_, *out_b = (u64*)out_b_, *ws = (u64*)workspace_;
   if (!level_ok(p, level) || level < 2 || !a3 || !b3 || !c3 || !key_b || !key_a || !out_a ||
@@ -1160,7 +1193,7 @@ int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const u
   Keys keys = keys_block((const u64*)key_b, (const u64*)key_a);
   keys.shared = true;  // one relinearisation key for the whole batch
   if (ck::fused_supported(p->logn) && p->fused && t.beta <= 8) {
-    const Relin rl{b3, c3};
+    const Relin rl{b3, c3, bc_stride};
     return keyswitch_fused(p, level, a3, nullptr, keys, 1, nullptr, 1, nullptr, &rl, out_a, out_b,
                            w, batch, st);
   }
@@ -1169,9 +1202,9 @@ int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const u
   CK_TRY(modup_impl(p, level, a3, w.dig, w.tmp, batch, st));
   CK_TRY(kskip_impl(p, level, w.dig, keys, 1, nullptr, w.uv, w.uv + R * N, 2 * R * N, batch, st));
   // pmodup (ckks.py:478-489): chain rows += [P]_q * x, special rows += 0
-  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv, 2 * R * N, w.uv, 2 * R * N, b3, l * N, nullptr, 0,
+  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv, 2 * R * N, w.uv, 2 * R * N, b3, bc_stride, nullptr, 0,
                 t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, batch, st));
-  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + R * N, 2 * R * N, w.uv + R * N, 2 * R * N, c3, l * N,
+  CK_TRY(ew_run(p, ck::EW_ADDMULC, w.uv + R * N, 2 * R * N, w.uv + R * N, 2 * R * N, c3, bc_stride,
                 nullptr, 0, t.d_chain_prime, t.d_pmod, 1, nullptr, (int)l, batch, st));
   // ModDown pair by P * q_last (ckks.py:643-651), u and v as one batch of 2B
   CK_TRY(moddown_core(p, m, w.uv, R * N, w.conv, 2 * batch, st));
@@ -1180,6 +1213,17 @@ int ck_relin(const ck_plan* p, const uint64_t* a3_, const uint64_t* b3_, const u
                 m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, batch, st));
   return ew_run(p, ck::EW_MODDOWN, out_b, lo * N, w.uv + R * N, 2 * R * N, w.conv + lo * N,
                 2 * lo * N, nullptr, 0, m.d_keep_prime, m.d_pinv, 1, nullptr, (int)lo, batch, st);
+}
+}  // namespace
+
+extern "C" {
+
+int ck_relin(const ck_plan* p, const uint64_t* a3, const uint64_t* b3, const uint64_t* c3,
+             const uint64_t* key_b, const uint64_t* key_a, int level, uint64_t* out_a,
+             uint64_t* out_b, uint64_t* workspace, int batch, ck_stream stream) {
+  const long long ln = p ? (long long)level * p->n : 0;
+  return relin_impl(p, a3, b3, c3, ln, key_b, key_a, level, out_a, out_b, workspace, batch,
+                    stream);
 }
 
 size_t ck_hrotate_workspace_bytes(const ck_plan* p, int level, int n_rot) {
