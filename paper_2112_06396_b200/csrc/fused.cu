@@ -74,6 +74,25 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const 
   __syncthreads();
   row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
 }
+// Primes below 2^54 (small_prime): approximate-quotient butterflies, no folding;
+// inputs below 16q, outputs below (16 + 4 P2) q < 2^60.
+template <int P2, int LOGN>
+__device__ CK_KS_DIGIT_INLINE void ks_digit_ntt_small(u64* srow, int g, int sr,
+                                                      const ulonglong2* tw, u64 q) {
+  u64 x[kE];
+  row_from_smem<P2, 0, false>(x, g, srow);
+  row_transform<P2, false, LOGN, SyncCta, true>(x, g, sr << P2, srow, tw, 0 - q, q << 2);
+  __syncthreads();
+  row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
+}
+#ifndef CKB200_SMALLQ
+#define CKB200_SMALLQ 1
+#endif
+template <int P2, int LOGN>
+CK_D void ks_digit_ntt_any(u64* srow, int g, int sr, const ulonglong2* tw, u64 q, u64 two_q) {
+  if (CKB200_SMALLQ && small_prime(q)) ks_digit_ntt_small<P2, LOGN>(srow, g, sr, tw, q);
+  else ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);
+}
 
 // ---------------------------------------------------------------- KSKIP row
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       else if (d == 1) cp_async_wait<(BETA >= 2 ? BETA - 2 : 0)>();
       else if (d == 2) cp_async_wait<(BETA >= 3 ? BETA - 3 : 0)>();
       else cp_async_wait<0>();
-      if (!own) ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);  // own rows are in place
+      if (!own) ks_digit_ntt_any<P2, LOGN>(srow, g, sr, tw, q, two_q);  // own rows are in place
     }
   } else {
 #pragma unroll 1
@@ -395,8 +414,10 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
     for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
     row_to_smem<P2, 0, false>(y, g, srow);
   }
-  ks_digit_ntt<P2, LOGN>(srow, g, r, tw, q, two_q);  // lazy [0,16q); q >= 2^56 canonical
-  constexpr bool lazy = LAZY;
+  ks_digit_ntt_any<P2, LOGN>(srow, g, r, tw, q, two_q);  // lazy [0,16q) (small primes [0,64q)); q >= 2^56 canonical
+  // LAZY instantiation: every kept prime is below 2^59; otherwise decide per row
+  const bool lazy = LAZY || q < ((u64)1 << 59);
+  const u64 qoff = CKB200_SMALLQ && small_prime(q) ? q << 6 : q << 4;
   __syncthreads();
 #else
   u64 y[kE];
@@ -418,7 +439,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
     const int c = sub_index<P2, 0, false>(g, k);
-    o[k] = lazy ? shoup(x[c] + (q << 4) - srow[sidx(c)], pinv.x, pinv.y, q)
+    o[k] = lazy ? shoup(x[c] + qoff - srow[sidx(c)], pinv.x, pinv.y, q)
                 : shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
   }
   const u64* addp = w ? a.addend : a.addend_u;

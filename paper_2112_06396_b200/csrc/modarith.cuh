@@ -118,6 +118,36 @@ CK_D void bfly_gs(u64& X, u64& Y, u64 w, u64 wp, u64 q, u64 two_q) {
   Y = shoup_tw(x - y + two_q, w, wp, q, two_q);
 }
 
+// ---- small-prime forward butterfly (q < 2^54) ----
+// Approximate Shoup quotient from three 32-bit products (the low x low product
+// and the carries of the cross terms are dropped): Q in [floor(y wp / 2^64) - 2,
+// floor(y wp / 2^64)], so t = y w - Q q lies in [0, 4q) for ANY 64-bit y.
+// With nq = 2^64 - q the remainder is one multiply-accumulate chain
+// (y w + Q nq mod 2^64), no negation.  Values grow by 4q per level and are
+// never folded: a row phase of up to 10 levels starting below 16q stays
+// below 56q < 2^60 (the bound the 30-bit-split key MAC needs).
+CK_D u64 shoup_tw4(u64 y, u64 w, u64 wp, u64 nq) {
+  // explicit 32-bit products (plain C++ makes nvcc emit 64-bit multiplies of the
+  // shifted halves and re-roll the unrolled butterfly loops around them)
+  u32 y0, y1, p0, p1, h1, h2;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(y0), "=r"(y1) : "l"(y));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(wp));
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(h1) : "r"(y0), "r"(p1));
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(h2) : "r"(y1), "r"(p0));
+  u64 Q;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(Q) : "r"(y1), "r"(p1));
+  Q += (u64)h1 + h2;
+  return y * w + Q * nq;
+}
+CK_D void bfly_ct4(u64& X, u64& Y, u64 w, u64 wp, u64 nq, u64 q4) {
+  const u64 t = shoup_tw4(Y, w, wp, nq);
+  const u64 xx = X;
+  X = xx + t;
+  Y = xx - t + q4;
+}
+// true when the no-fold forward row phase applies to this prime
+CK_D bool small_prime(u64 q) { return (q >> 54) == 0; }
+
 // ---- index helpers ----
 CK_D u32 brev_bits(u32 x, int bits) { return bits ? (__brev(x) >> (32 - bits)) : 0u; }
 

@@ -74,9 +74,12 @@ CK_D int sub_index(int g, int r) {
 // by 2q per stage to < 16q < 2^64 (q < 2^60); the caller folds them back
 // with one csub(8q) per element per pass (fwd_fold) -- half the ALU work of
 // Harvey's per-butterfly correction.
-template <int P, int p, bool INV, bool TW_SMEM, int LOGN, int JSHIFT>
+// SMALL (forward only, q < 2^54): approximate-quotient butterflies without any
+// range folding (modarith.cuh bfly_ct4); q / two_q then carry 2^64 - q / 4q.
+template <int P, int p, bool INV, bool TW_SMEM, int LOGN, int JSHIFT, bool SMALL = false>
 CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict__ tw, u64 q,
                    u64 two_q) {
+  static_assert(!(SMALL && INV), "small-prime variant is forward only");
   constexpr int C = Sched<P>::C(p);
   constexpr int LD = Sched<P>::logD(p, INV);
   constexpr int NG = kE >> C;
@@ -104,6 +107,8 @@ CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict_
           u64& Y = x[(h << C) + k + half];
           if (INV) {
             bfly_gs(X, Y, w.x, w.y, q, two_q);
+          } else if (SMALL) {
+            bfly_ct4(X, Y, w.x, w.y, q, two_q);
           } else {
             const u64 t = shoup_tw(Y, w.x, w.y, q, two_q);
             const u64 xx = X;
@@ -175,13 +180,13 @@ CK_D void bar_arrive_n(int id, int nt) {
 // the partner's result.  Values stay in the pass-1 layout (RowLast<9> = 1).
 CK_D u64 shfl_xor64(u64 v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 
-template <int P, bool INV, int LOGN>
+template <int P, bool INV, int LOGN, bool SMALL = false>
 CK_D void last_level_shfl(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict__ tw,
                           u64 q, u64 two_q) {
   static_assert(P == 9 && kE == 16, "512-point rows: 32 threads = one warp per row");
   constexpr int X = INV ? 16 : 1;  // lane distance of the partner
   const bool lower = (g & X) == 0;  // holds the pairs' first (lower-index) elements
-  if (!INV) fwd_fold(x, q << 3);
+  if (!INV && !SMALL) fwd_fold(x, q << 3);
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const u64 recv = shfl_xor64(lower ? x[kk + 8] : x[kk], X);
@@ -191,10 +196,14 @@ CK_D void last_level_shfl(u64 (&x)[kE], int g, int jbase, const ulonglong2* __re
     const int j = jbase + sub_index<P, 1, INV>(g & ~X, k);
     if (!INV) {
       const ulonglong2 w = __ldg(tw + (1 << (LOGN - 1)) + (j >> 1));
-      const u64 t = shoup_tw(yv, w.x, w.y, q, two_q);
-      const u64 xx = xv;
-      xv = xx + t;
-      yv = xx - t + two_q;
+      if (SMALL) {
+        bfly_ct4(xv, yv, w.x, w.y, q, two_q);
+      } else {
+        const u64 t = shoup_tw(yv, w.x, w.y, q, two_q);
+        const u64 xx = xv;
+        xv = xx + t;
+        yv = xx - t + two_q;
+      }
     } else {
       const ulonglong2 w = __ldg(tw + (1 << (LOGN - 9)) + (j >> 9));
       bfly_gs(xv, yv, w.x, w.y, q, two_q);
@@ -216,30 +225,33 @@ struct RowLast {
   static constexpr int value = P == 9 ? 1 : Sched<P>::np - 1;
 };
 
-template <int P2, bool INV, int LOGN, class Sync = SyncCta>
+// SMALL (forward, q < 2^54): inputs below 16q, outputs below (16 + 4 P2) q, no
+// folding; pass 2^64 - q and 4q in place of q and 2q.
+template <int P2, bool INV, int LOGN, class Sync = SyncCta, bool SMALL = false>
 CK_D void row_transform(u64 (&x)[kE], int g, int jbase, u64* srow,
                         const ulonglong2* __restrict__ tw, u64 q, u64 two_q) {
   constexpr int NP = Sched<P2>::np;
   static_assert(NP <= 3, "row too long");
-  if (!INV) fwd_fold(x, q << 3);
-  run_pass<P2, 0, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
+  constexpr bool FOLD = !INV && !SMALL;
+  if (FOLD) fwd_fold(x, q << 3);
+  run_pass<P2, 0, INV, false, LOGN, 0, SMALL>(x, g, jbase, tw, q, two_q);
   if constexpr (NP > 1) {
     Sync::sync();
     row_to_smem<P2, 0, INV>(x, g, srow);
     Sync::sync();
     row_from_smem<P2, 1, INV>(x, g, srow);
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass<P2, 1, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
+    if (FOLD) fwd_fold(x, q << 3);
+    run_pass<P2, 1, INV, false, LOGN, 0, SMALL>(x, g, jbase, tw, q, two_q);
   }
   if constexpr (P2 == 9) {
-    last_level_shfl<P2, INV, LOGN>(x, g, jbase, tw, q, two_q);
+    last_level_shfl<P2, INV, LOGN, SMALL>(x, g, jbase, tw, q, two_q);
   } else if constexpr (NP > 2) {
     Sync::sync();
     row_to_smem<P2, 1, INV>(x, g, srow);
     Sync::sync();
     row_from_smem<P2, 2, INV>(x, g, srow);
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass<P2, 2, INV, false, LOGN, 0>(x, g, jbase, tw, q, two_q);
+    if (FOLD) fwd_fold(x, q << 3);
+    run_pass<P2, 2, INV, false, LOGN, 0, SMALL>(x, g, jbase, tw, q, two_q);
   }
 }
 
