@@ -145,8 +145,18 @@ CK_D void bfly_ct4(u64& X, u64& Y, u64 w, u64 wp, u64 nq, u64 q4) {
   X = xx + t;
   Y = xx - t + q4;
 }
+// Inverse (Gentleman-Sande) counterpart: no conditional subtraction on the sum, so
+// values double per level (inputs of level k below 2^(k+1) q, B = 2^(k+1) q keeps the
+// difference non-negative); the product is back in [0, 4q).
+CK_D void bfly_gs4(u64& X, u64& Y, u64 w, u64 wp, u64 nq, u64 B) {
+  const u64 x = X, y = Y;
+  X = x + y;
+  Y = shoup_tw4(x - y + B, w, wp, nq);
+}
 // true when the no-fold forward row phase applies to this prime
 CK_D bool small_prime(u64 q) { return (q >> 54) == 0; }
+// ... and the no-fold inverse row phase of 2^P2-point rows (outputs below 2^(P2+1) q)
+CK_D bool small_prime_inv(u64 q, int p2) { return small_prime(q) && (q >> (63 - p2)) == 0; }
 
 // ---- index helpers ----
 CK_D u32 brev_bits(u32 x, int bits) { return bits ? (__brev(x) >> (32 - bits)) : 0u; }

@@ -82,6 +82,9 @@ struct RowCfg {
   static constexpr int RS = S + S / 16;  // padded smem row stride
 };
 
+#ifndef CKB200_SMALLQ
+#define CKB200_SMALLQ 1
+#endif
 template <int P1, int P2, bool INV>
 __global__ void __launch_bounds__(256, CKB200_NTT_MINB)
 ntt_row_kernel(NttArgs a) {
@@ -117,36 +120,32 @@ ntt_row_kernel(NttArgs a) {
 #pragma unroll
     for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 0, INV>(g, r))];
   }
-  if (!INV) fwd_fold(x, q << 3);
-  run_pass<P2, 0, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
-  if constexpr (NP > 1) {
-    __syncthreads();
+  // primes below 2^54: approximate-quotient butterflies without range folding
+  // (ntt.cuh SMALL); inverse outputs are then below 2^(P2+1) q: the tensor-core
+  // column phase takes any 64-bit operand, the butterfly column kernel needs [0, 2q)
+  const bool small = CKB200_SMALLQ && (INV ? small_prime_inv(q, P2) : small_prime(q));
+  if (small) {
+    row_transform<P2, INV, P1 + P2, SyncCta, true>(x, g, jbase, srow, tw, 0 - q, INV ? q : q << 2);
+    if (INV && !(P1 == 8 && a.tcB && a.tcD)) {
+      const PrimeConst& Pc = a.pc[prime];
 #pragma unroll
-    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, 0, INV>(g, r))] = x[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 1, INV>(g, r))];
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass<P2, 1, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
-  }
-  if constexpr (P2 == 9) {
-    last_level_shfl<P2, INV, P1 + P2>(x, g, jbase, tw, q, two_q);
-  } else if constexpr (NP > 2) {
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, 1, INV>(g, r))] = x[r];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = srow[sidx(sub_index<P2, 2, INV>(g, r))];
-    if (!INV) fwd_fold(x, q << 3);
-    run_pass<P2, 2, INV, false, P1 + P2, 0>(x, g, jbase, tw, q, two_q);
+      for (int r = 0; r < kE; ++r) x[r] = red64_lazy(x[r], Pc);
+    }
+  } else {
+    row_transform<P2, INV, P1 + P2>(x, g, jbase, srow, tw, q, two_q);
   }
   static_assert(NP <= 3, "sub-transform too large");
   if (!INV) {
     // end of the forward transform: canonical residues; stores staged
     // through smem so the global writes are coalesced
+    if (small) {  // below (16 + 4 P2) q: one Barrett step
+      const PrimeConst& Pc = a.pc[prime];
 #pragma unroll
-    for (int r = 0; r < kE; ++r) x[r] = fwd_final(x[r], q);
+      for (int r = 0; r < kE; ++r) x[r] = red64(x[r], Pc);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kE; ++r) x[r] = fwd_final(x[r], q);
+    }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kE; ++r) srow[sidx(sub_index<P2, RowLast<P2>::value, INV>(g, r))] = x[r];

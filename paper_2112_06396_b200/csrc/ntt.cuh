@@ -74,12 +74,13 @@ CK_D int sub_index(int g, int r) {
 // by 2q per stage to < 16q < 2^64 (q < 2^60); the caller folds them back
 // with one csub(8q) per element per pass (fwd_fold) -- half the ALU work of
 // Harvey's per-butterfly correction.
-// SMALL (forward only, q < 2^54): approximate-quotient butterflies without any
-// range folding (modarith.cuh bfly_ct4); q / two_q then carry 2^64 - q / 4q.
+// SMALL (row phases, q < 2^54): approximate-quotient butterflies without any
+// range folding (modarith.cuh bfly_ct4 / bfly_gs4); q / two_q then carry
+// 2^64 - q and 4q (forward) or q (inverse; inputs below 2q).
 template <int P, int p, bool INV, bool TW_SMEM, int LOGN, int JSHIFT, bool SMALL = false>
 CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict__ tw, u64 q,
                    u64 two_q) {
-  static_assert(!(SMALL && INV), "small-prime variant is forward only");
+  static_assert(!SMALL || JSHIFT == 0, "small-prime variant: row phases only");
   constexpr int C = Sched<P>::C(p);
   constexpr int LD = Sched<P>::logD(p, INV);
   constexpr int NG = kE >> C;
@@ -105,7 +106,9 @@ CK_D void run_pass(u64 (&x)[kE], int g, int jbase, const ulonglong2* __restrict_
         for (int k = k0; k < k0 + half; ++k) {
           u64& X = x[(h << C) + k];
           u64& Y = x[(h << C) + k + half];
-          if (INV) {
+          if (INV && SMALL) {
+            bfly_gs4(X, Y, w.x, w.y, q, two_q << (LD + lhalf + 1));
+          } else if (INV) {
             bfly_gs(X, Y, w.x, w.y, q, two_q);
           } else if (SMALL) {
             bfly_ct4(X, Y, w.x, w.y, q, two_q);
@@ -206,7 +209,8 @@ CK_D void last_level_shfl(u64 (&x)[kE], int g, int jbase, const ulonglong2* __re
       }
     } else {
       const ulonglong2 w = __ldg(tw + (1 << (LOGN - 9)) + (j >> 9));
-      bfly_gs(xv, yv, w.x, w.y, q, two_q);
+      if (SMALL) bfly_gs4(xv, yv, w.x, w.y, q, two_q << 9);
+      else bfly_gs(xv, yv, w.x, w.y, q, two_q);
     }
     const u64 back = shfl_xor64(lower ? yv : xv, X);
     if (lower) {
