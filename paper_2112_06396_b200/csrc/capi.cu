@@ -258,6 +258,10 @@ PrimeConst make_pc(u64 q, int logn) {
   P.ninv = invmod_h(((u64)1 << logn) % q, q);
   P.ninvp = shoup_h(P.ninv, q);
   P.nq = (u64)0 - q;
+  int bl = 0;
+  while (bl < 64 && (q >> bl)) ++bl;
+  P.sh = (u64)(bl - 1);
+  P.mu = (u64)(((u128)1 << (P.sh + 64)) / q);  // q is not a power of two: < 2^64
   return P;
 }
 
@@ -812,6 +816,7 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
   ka_.logn = p->logn;
   ka_.key_prefetch = p->key_prefetch;
   ka_.row0 = 0;
+  ka_.lazy_keep = (int)keep;  // the kept rows go to md_row only
   CK_TRY(ck::launch_ks_row(ka_, (int)R, B, st));
   if (relin) {
     // pmodup (ckks.py:478-489) on the dropped chain row q_last: it feeds the BC

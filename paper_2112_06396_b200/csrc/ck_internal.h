@@ -10,7 +10,7 @@
 #else
 typedef unsigned long long u64;
 struct PrimeConst {
-  u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, nq;
+  u64 q, two_q, bar, c30, c30p, c60, c60p, r64, r64p, ninv, ninvp, nq, mu, sh;
 };
 #endif
 
@@ -89,6 +89,8 @@ struct KsRowArgs {
   int beta, l, R, logn;
   int key_prefetch;             // bulk L2 prefetch of the first k/8 of each key tile at kernel start
   int row0;                     // first raised row of the launch (grid.z = rows from row0)
+  int lazy_keep;                // rows i < lazy_keep with q < 2^59 may stay in [0, 3q): md_row's lazy
+                                // epilogue (x + c q - conv, then a Shoup product) takes them as they are
 };
 int launch_ks_row(const KsRowArgs& a, int rows, int batch, cudaStream_t st);
 

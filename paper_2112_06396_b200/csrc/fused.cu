@@ -94,6 +94,12 @@ CK_D void ks_digit_ntt_any(u64* srow, int g, int sr, const ulonglong2* tw, u64 q
   else ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);
 }
 
+// KSKIP output: canonical, or [0, 3q) where the consumer takes lazy values
+CK_D u64 ks_out(const Acc3& s, const PrimeConst& P, bool lazy) {
+  const u64 r = acc3_reduce_lazy(s, P);
+  return lazy ? r : csub(csub(r, P.two_q), P.q);
+}
+
 // ---------------------------------------------------------------- KSKIP row
 // BETA > 0: compile-time digit count (fully unrolled inner product, so the
 // 2*BETA key loads of an element are independent and stay in flight);
@@ -227,6 +233,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
   // reduction constants in registers for the MAC loop only (loaded after the
   // NTTs: a reference into global memory would reload them after every store)
   const PrimeConst P = Pg;
+  const bool lazy_out = i < a.lazy_keep && q < ((u64)1 << 59);  // [0, 3q) for md_row
   const long long tile0 = (long long)blockIdx.x * F::TR << P2;
   const u64* ka = key_block(a.key_a, a.key_a_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
   const u64* kb = key_block(a.key_b, a.key_b_ptrs, a.key_batch, b) + ((long long)prime << LOGN) + tile0;
@@ -271,8 +278,8 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
         }
       }
       u64* uw = ubase + tile0 + e;
-      *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
-      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+      *(ulonglong2*)uw = make_ulonglong2(ks_out(su[0], P, lazy_out), ks_out(su[1], P, lazy_out));
+      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(ks_out(sv[0], P, lazy_out), ks_out(sv[1], P, lazy_out));
       __syncthreads();  // every thread is done with slot sl
       if (threadIdx.x == 0 && m + NSK < ITER) ring_issue(m + NSK);
     }
@@ -322,8 +329,8 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
         }
       }
       u64* uw = ubase + tile0 + e;
-      *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
-      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+      *(ulonglong2*)uw = make_ulonglong2(ks_out(su[0], P, lazy_out), ks_out(su[1], P, lazy_out));
+      *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(ks_out(sv[0], P, lazy_out), ks_out(sv[1], P, lazy_out));
       if (m + 1 < ITER) {
 #pragma unroll
         for (int d = 0; d < BETA; ++d) {
@@ -365,8 +372,8 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       }
     }
     u64* uw = ubase + tile0 + e;
-    *(ulonglong2*)uw = make_ulonglong2(acc3_reduce(su[0], P), acc3_reduce(su[1], P));
-    *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(acc3_reduce(sv[0], P), acc3_reduce(sv[1], P));
+    *(ulonglong2*)uw = make_ulonglong2(ks_out(su[0], P, lazy_out), ks_out(su[1], P, lazy_out));
+    *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(ks_out(sv[0], P, lazy_out), ks_out(sv[1], P, lazy_out));
   }
   }
 }

@@ -26,6 +26,8 @@ struct PrimeConst {
   u64 r64, r64p;  // 2^64 mod q, Shoup companion
   u64 ninv, ninvp;
   u64 nq;         // 2^64 - q
+  u64 mu;         // floor(2^(sh + 64) / q), sh = bitlen(q) - 1   (128-bit Barrett, acc3_reduce)
+  u64 sh;
 };
 
 CK_D u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }
@@ -91,16 +93,25 @@ CK_D void acc3_mac(Acc3& s, u32 a0, u32 a1, u32 b0, u32 b1) {
 CK_D u32 lo30(u64 x) { return (u32)x & 0x3fffffffu; }
 CK_D u32 hi30(u64 x) { return (u32)(x >> 30); }
 
-// Reduce lo + mid*2^30 + hi*2^60 into [0, q): assemble the exact 128-bit
-// value with funnel shifts and carries (ALU pipe), then one 128-bit
-// reduction (2 Shoup-style steps on the IMAD pipe instead of 3).
-CK_D u64 acc3_reduce(const Acc3& s, const PrimeConst& P) {
+// Reduce V = lo + mid*2^30 + hi*2^60 (V < 2^64 * 2^sh, i.e. at most 8 products of a
+// value below 2^60 with a residue): assemble the exact 128-bit value with funnel
+// shifts and carries (ALU pipe), then ONE Barrett step on its top 64 bits:
+//   Vt = floor(V / 2^sh), Q = floor(Vt mu / 2^64) in (V/q - 3, V/q]
+// (dropped bits of V: < 2^sh/q <= 1; mu's floor: Vt/2^64 < 1; the last floor: < 1),
+// so V - Q q (mod 2^64) lies in [0, 3q).  One 64-bit high product and one low
+// product instead of the two Shoup-style steps of red128.
+CK_D u64 acc3_reduce_lazy(const Acc3& s, const PrimeConst& P) {
   u64 lo = s.lo, hi = 0;
   const u64 m_lo = s.mid << 30, m_hi = s.mid >> 34;
   const u64 h_lo = s.hi << 60, h_hi = s.hi >> 4;
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(m_lo), "l"(m_hi));
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(h_lo), "l"(h_hi));
-  return red128(hi, lo, P);
+  const int sh = (int)P.sh;  // 49 .. 59
+  const u64 vt = (hi << (64 - sh)) | (lo >> sh);
+  return lo - mulhi64(vt, P.mu) * P.q;
+}
+CK_D u64 acc3_reduce(const Acc3& s, const PrimeConst& P) {
+  return csub(csub(acc3_reduce_lazy(s, P), P.two_q), P.q);
 }
 
 // ---- NTT butterflies (Harvey lazy) ----
