@@ -81,7 +81,7 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt_small(u64* srow, int g, int sr,
                                                       const ulonglong2* tw, u64 q) {
   u64 x[kE];
   row_from_smem<P2, 0, false>(x, g, srow);
-  row_transform<P2, false, LOGN, SyncCta, true>(x, g, sr << P2, srow, tw, 0 - q, q << 2);
+  row_transform<P2, false, LOGN, SyncCta, true>(x, g, sr << P2, srow, tw, neg_opaque(q), q << 2);
   __syncthreads();
   row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
 }

@@ -150,6 +150,13 @@ CK_D u64 shoup_tw4(u64 y, u64 w, u64 wp, u64 nq) {
   Q += (u64)h1 + h2;
   return y * w + Q * nq;
 }
+// 2^64 - q as a value the compiler cannot see through (it would otherwise rewrite
+// Q * (0 - q) as -(Q * q) and undo the single multiply-accumulate chain)
+CK_D u64 neg_opaque(u64 q) {
+  u64 r = 0 - q;
+  asm("mov.b64 %0, %0;" : "+l"(r));
+  return r;
+}
 CK_D void bfly_ct4(u64& X, u64& Y, u64 w, u64 wp, u64 nq, u64 q4) {
   const u64 t = shoup_tw4(Y, w, wp, nq);
   const u64 xx = X;

@@ -125,7 +125,7 @@ ntt_row_kernel(NttArgs a) {
   // column phase takes any 64-bit operand, the butterfly column kernel needs [0, 2q)
   const bool small = CKB200_SMALLQ && (INV ? small_prime_inv(q, P2) : small_prime(q));
   if (small) {
-    row_transform<P2, INV, P1 + P2, SyncCta, true>(x, g, jbase, srow, tw, 0 - q, INV ? q : q << 2);
+    row_transform<P2, INV, P1 + P2, SyncCta, true>(x, g, jbase, srow, tw, neg_opaque(q), INV ? q : q << 2);
     if (INV && !(P1 == 8 && a.tcB && a.tcD)) {
       const PrimeConst& Pc = a.pc[prime];
 #pragma unroll

@@ -115,43 +115,32 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // < 0.51; the floor: < 1), so V - qh p + p lands in (0, 4p), computed mod 2^64.
 // One mul.hi replaces the FP64 estimate (whose DADD/DFMA bursts throttled the
 // FP64 pipe in every epilogue); the byte-plane assembly stays on the ALU pipe.
+// The byte-plane assembly is written so that ptxas keeps it on the ALU pipe (the
+// fma-heavy pipe is this kernel's limiter and ptxas otherwise turns shift-adds and
+// register moves into IMADs): planes are below 2^24, so s << 8 is a rotate
+// (funnel shift, never an IMAD), and the 16-bit alignments are rotate + mask.
+__device__ __forceinline__ u32 rotl32(u32 x, int n) {
+  u32 r;
+  asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
+}
 __device__ __forceinline__ u64 reduce_lazy(const uint32_t* s, u64 p, u32 m81) {
-  const u32 P0 = s[0] + (s[1] << 8), P1 = s[2] + (s[3] << 8);
-  const u32 P2 = s[4] + (s[5] << 8), P3 = s[6] + (s[7] << 8);
-  u32 lo, hi, ml, mh;
-  // vlo = P0 + P1 2^16 + P2 2^32 + P3 2^48 (mod 2^64)
-  asm("{\n\t.reg .u32 t0, t1;\n\t"
-      "shl.b32 t0, %2, 16;\n\t"
-      "shr.u32 t1, %2, 16;\n\t"
-      "add.cc.u32 %0, %3, t0;\n\t"
-      "shl.b32 t0, %5, 16;\n\t"
-      "addc.u32 %1, %4, t0;\n\t"
-      "add.u32 %1, %1, t1;\n\t}"
-      : "=r"(lo), "=r"(hi)
-      : "r"(P1), "r"(P0), "r"(P2), "r"(P3));
-  // vhi = P3 2^16 + P2 < 2^49
-  asm("{\n\t.reg .u32 t0;\n\t"
-      "shl.b32 t0, %2, 16;\n\t"
-      "add.cc.u32 %0, %3, t0;\n\t"
-      "shr.u32 t0, %2, 16;\n\t"
-      "addc.u32 %1, t0, 0;\n\t}"
-      : "=r"(ml), "=r"(mh)
-      : "r"(P3), "r"(P2));
-  const u32 qh = __umulhi(__funnelshift_r(ml, mh, 17), m81);
-  // r = vlo + p - qh p  (mod 2^64)
-  const u32 pl = (u32)p, ph = (u32)(p >> 32);
-  u32 rl, rh;
-  asm("{\n\t.reg .u32 m0, m1;\n\t"
-      "mul.lo.u32 m0, %4, %2;\n\t"
-      "mul.hi.u32 m1, %4, %2;\n\t"
-      "mad.lo.u32 m1, %4, %3, m1;\n\t"
-      "add.cc.u32 %0, %5, %2;\n\t"
-      "addc.u32 %1, %6, %3;\n\t"
-      "sub.cc.u32 %0, %0, m0;\n\t"
-      "subc.u32 %1, %1, m1;\n\t}"
-      : "=r"(rl), "=r"(rh)
-      : "r"(pl), "r"(ph), "r"(qh), "r"(lo), "r"(hi));
-  return ((u64)rh << 32) | rl;
+  const u32 P0 = s[0] + rotl32(s[1], 8), P1 = s[2] + rotl32(s[3], 8);
+  const u32 P2 = s[4] + rotl32(s[5], 8), P3 = s[6] + rotl32(s[7], 8);  // < 2^32
+  // V = P0 + P1 2^16 + P2 2^32 + P3 2^48 = lo + hi 2^32 + top 2^64
+  const u32 r1 = rotl32(P1, 16), r3 = rotl32(P3, 16);
+  const u32 a_lo = r1 & 0xffff0000u, a_hi = r1 & 0xffffu;
+  const u32 b_lo = r3 & 0xffff0000u, b_hi = r3 & 0xffffu;
+  u32 lo, hi, top;
+  asm("add.cc.u32 %0, %1, %2;" : "=r"(lo) : "r"(P0), "r"(a_lo));
+  asm("addc.cc.u32 %0, %1, %2;" : "=r"(hi) : "r"(P2), "r"(a_hi));
+  asm("addc.u32 %0, %1, 0;" : "=r"(top) : "r"(b_hi));
+  asm("add.cc.u32 %0, %0, %1;" : "+r"(hi) : "r"(b_lo));
+  asm("addc.u32 %0, %0, 0;" : "+r"(top));
+  // vhi = floor(V / 2^32) = hi + top 2^32 < 2^49, W = floor(vhi / 2^17)
+  const u32 qh = __umulhi(__funnelshift_r(hi, top, 17), m81);
+  const u64 v = ((u64)hi << 32) | lo;
+  return v + p - (u64)qh * p;  // (mod 2^64)
 }
 
 // round(2^81 / p) for reduce_lazy (p > 2^49.5: < 2^31.5)
@@ -159,42 +148,12 @@ __device__ __forceinline__ u32 tc_m81(u64 p) {
   return (u32)__double2uint_rn(__ddiv_rn(2417851639229258349412352.0, (double)p));
 }
 
-// x * w mod p into [0, 4p) for x < 2^56, w < p, wp = floor(w 2^64 / p): Shoup
-// with a 3-product quotient q1 = xh wph + hi(xh wpl) + hi(xl wph) (xh = x >> 32)
-// that undershoots floor(x wp / 2^64) by at most 2 (two dropped fractional
-// carries + the dropped xl wpl term), so the remainder grows by at most 2p.
+// x * w mod p into [0, 4p) for any 64-bit x: the approximate-quotient Shoup product
+// of the small-prime butterflies (modarith.cuh shoup_tw4: three 32-bit products for
+// the quotient, the remainder as one multiply-accumulate chain with 2^64 - p).
 // The next tensor-core pass accepts any 64-bit operand; canonical outputs
 // fold it with two conditional subtractions.
-__device__ __forceinline__ u64 shoup_tc(u64 x, u64 w, u64 wp, u64 p) {
-  const u32 xl = (u32)x, xh = (u32)(x >> 32);
-  const u32 wl = (u32)w, wh = (u32)(w >> 32);
-  const u32 wpl = (u32)wp, wph = (u32)(wp >> 32);
-  const u32 pl = (u32)p, ph = (u32)(p >> 32);
-  u32 rl, rh;
-  asm("{\n\t.reg .u32 q0, q1, a, b, c0, c1;\n\t"
-      // q1 = xh * wph + hi(xh * wpl) + hi(xl * wph)  (64-bit)
-      "mul.hi.u32 a, %3, %7;\n\t"
-      "mul.hi.u32 b, %2, %8;\n\t"
-      "mad.lo.cc.u32 q0, %3, %8, a;\n\t"
-      "madc.hi.u32 q1, %3, %8, 0;\n\t"
-      "add.cc.u32 q0, q0, b;\n\t"
-      "addc.u32 q1, q1, 0;\n\t"
-      // x * w (mod 2^64)
-      "mul.lo.u32 c0, %2, %4;\n\t"
-      "mul.hi.u32 c1, %2, %4;\n\t"
-      "mad.lo.u32 c1, %2, %5, c1;\n\t"
-      "mad.lo.u32 c1, %3, %4, c1;\n\t"
-      // - q1 * p (mod 2^64)
-      "mul.lo.u32 a, q0, %9;\n\t"
-      "mul.hi.u32 b, q0, %9;\n\t"
-      "mad.lo.u32 b, q0, %10, b;\n\t"
-      "mad.lo.u32 b, q1, %9, b;\n\t"
-      "sub.cc.u32 %0, c0, a;\n\t"
-      "subc.u32 %1, c1, b;\n\t}"
-      : "=r"(rl), "=r"(rh)
-      : "r"(xl), "r"(xh), "r"(wl), "r"(wh), "r"(0), "r"(wpl), "r"(wph), "r"(pl), "r"(ph));
-  return ((u64)rh << 32) | rl;
-}
+__device__ __forceinline__ u64 shoup_tc(u64 x, u64 w, u64 wp, u64 np) { return shoup_tw4(x, w, wp, np); }
 
 __device__ __forceinline__ void st_u64(unsigned char* base, int row, int elem, u64 v) {
   *(u64*)(base + kmaj_off(row, elem * 8)) = v;
@@ -241,6 +200,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   const int prime = a.prime_idx[job];
   const u64 p = a.pc[prime].q;
   const u32 m81 = tc_m81(p);
+  const u64 np = neg_opaque(p);
   u64* base = a.data + (a.row_off ? a.row_off[job] : ((long long)job << a.logn)) +
               (long long)blockIdx.z * a.batch_stride;
   const unsigned mb_s = (unsigned)__cvta_generic_to_shared(mbar + grp);
@@ -315,7 +275,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
           const int o = h * 4 + u;                      // pass-1 output index
           const u64 y = reduce_lazy(sv + 8 * u, p, m81);
           const ulonglong2 d = tw[o * 16 + g1];
-          st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, p));  // [0, 4p)
+          st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, np));  // [0, 4p)
         }
       }
     }
@@ -347,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
           const int o2 = h * 4 + u;
           const u64 v = reduce_lazy(sv + 8 * u, p, m81);
           if (INV)  // rows 16 o2 + o1; canonical (the base conversion needs exact residues)
-            col[(long long)(o2 * 16 + o1) << P2] = csub(csub(shoup_tc(v, scl.x, scl.y, p), 2 * p), p);
+            col[(long long)(o2 * 16 + o1) << P2] = csub(csub(shoup_tc(v, scl.x, scl.y, np), 2 * p), p);
           else      // rows 16 o1 + o2; lazy (0, 4p)
             col[(long long)(o1 * 16 + o2) << P2] = v;
         }
