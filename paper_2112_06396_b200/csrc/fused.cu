@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
 // ------------------------------------------------------------ ModDown row
 template <int P1, int P2, bool LAZY>
 #ifndef CKB200_MD_MINB
-#define CKB200_MD_MINB 8
+#define CKB200_MD_MINB 6
 #endif
 #ifndef CKB200_MD_CALL
 #define CKB200_MD_CALL 1

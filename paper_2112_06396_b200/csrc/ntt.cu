@@ -12,7 +12,7 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 // ------------------------------------------------------------ column phase
 // grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
 #ifndef CKB200_NTT_MINB
-#define CKB200_NTT_MINB 3
+#define CKB200_NTT_MINB 4
 #endif
 template <int P1, int P2, bool INV>
 __global__ void __launch_bounds__(col_tc<P1>() * (1 << P1) / kE, CKB200_NTT_MINB)
