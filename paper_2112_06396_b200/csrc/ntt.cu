@@ -12,7 +12,12 @@ CK_D long long job_offset(const NttArgs& a, int job, int bz) {
 // ------------------------------------------------------------ column phase
 // grid = (2^P2 / kTC, jobs, batch); block = kTC * 2^P1 / kE
 #ifndef CKB200_NTT_MINB
-#define CKB200_NTT_MINB 4
+#define CKB200_NTT_MINB 3
+#endif
+// row kernel: 4 CTAs/SM (64 registers) for rows up to 256 points -- measured +0.5% on
+// C3 with the small-prime butterflies; longer rows spill there and stay at 3
+#ifndef CKB200_NTT_ROW_MINB
+#define CKB200_NTT_ROW_MINB 4
 #endif
 template <int P1, int P2, bool INV>
 __global__ void __launch_bounds__(col_tc<P1>() * (1 << P1) / kE, CKB200_NTT_MINB)
@@ -86,7 +91,7 @@ struct RowCfg {
 #define CKB200_SMALLQ 1
 #endif
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(256, CKB200_NTT_MINB)
+__global__ void __launch_bounds__(256, P2 <= 8 ? CKB200_NTT_ROW_MINB : CKB200_NTT_MINB)
 ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;
