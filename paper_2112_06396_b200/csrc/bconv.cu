@@ -20,6 +20,9 @@
 // The float estimate replicates numpy's op order with explicit _rn
 // intrinsics (no FMA contraction), round-half-even via rint().
 #include "ck_internal.h"
+#include "tc5.cuh"
+
+#include <algorithm>
 
 namespace ck {
 
@@ -355,6 +358,285 @@ static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
   launch_pdl(bconv_tc_kernel<KS>, grid, dim3(kTcWarps * 32), smem, st, G);
 }
 
+
+// ---------------------------------------------------------------------------
+// tcgen05 form (default for rings of at least 128 coefficients): the same exact
+// byte-sliced contraction as bconv_tc_kernel, on the 5th-generation tensor cores
+// with the accumulators in TMEM.
+//   A = [128 coefficients][Kp bytes]: byte a of source i at k = 8 i + a -- the u64
+//       residues themselves, copied by 8-byte cp.async into the canonical K-major
+//       operand layout (no repacking); Kp = 8 ns rounded up to the 32-byte K step.
+//   B = [N = 8 NC rows (target jj, plane b)][Kp]: byte b of T_ij 2^(8a) mod p_j for
+//       a chunk of NC <= 16 targets (tcgen05.mma M128, N = 8 NC, K32 steps).
+//   D = 128 TMEM lanes (coefficients) x N columns of s32 planes.
+// Epilogue: thread = coefficient (TMEM lane); per target the 8 planes are
+// assembled on the ALU pipe (tc5::assemble_planes), reduced with the integer
+// quotient of bconv_tc_kernel, corrected by k Q (centered), and stored -- a warp
+// writes 256 contiguous bytes of one target row.
+// One CTA per SM = 4 independent 8-warp pipelines (own double-buffered A operand,
+// own 128 TMEM columns and mbarrier), sharing B and the per-target constants; a
+// pipeline walks its tiles, the next tile's sources streaming in during the
+// epilogues; the two warps of a TMEM lane quarter split each chunk's targets.
+constexpr int kT5Groups = 4, kT5GW = 8, kT5Threads = 32 * kT5GW * kT5Groups;
+constexpr int kT5Rows = 128;
+#ifndef CKB200_T5_TILES
+#define CKB200_T5_TILES 32
+#endif
+constexpr int kT5Tiles = CKB200_T5_TILES;  // tiles per CTA (B and the constants loaded once)
+
+struct T5Shape {
+  int kp, nc, nchunk;
+};
+__host__ __device__ inline T5Shape t5_shape(int ns, int nd) {
+  T5Shape s;
+  s.kp = ((8 * ns + 31) / 32) * 32;
+  s.nchunk = (nd + 15) / 16;
+  s.nc = (nd + s.nchunk - 1) / s.nchunk;
+  s.nc = (s.nc + 3) & ~3;                 // N = 8 nc a multiple of 32: each half of a chunk is whole pairs
+  return s;
+}
+size_t bconv_t5_table_bytes(int ns, int nd) {
+  const T5Shape s = t5_shape(ns, nd);
+  return (size_t)s.nchunk * 8 * s.nc * s.kp;
+}
+// Host: B5[chunk][n = 8 jj + b][k = 8 i + a] in operand layout; Tp[(i*8 + a)*nd + j] =
+// T_ij 2^(8a) mod p_j.
+void bconv_t5_table(const u64* Tp, int ns, int nd, unsigned char* B5) {
+  const T5Shape s = t5_shape(ns, nd);
+  for (int c = 0; c < s.nchunk; ++c)
+    for (int jj = 0; jj < s.nc; ++jj)
+      for (int b = 0; b < 8; ++b)
+        for (int k = 0; k < s.kp; ++k) {
+          const int j = c * s.nc + jj, i = k >> 3, a = k & 7;
+          unsigned char v = 0;
+          if (j < nd && i < ns) v = (unsigned char)(Tp[((size_t)i * 8 + a) * nd + j] >> (8 * b));
+          B5[(size_t)c * 8 * s.nc * s.kp + tc5::kmaj_off(8 * jj + b, k, s.kp)] = v;
+        }
+}
+
+template <int NT>
+struct T5Ld;
+template <>
+struct T5Ld<4> {
+  uint32_t v[32];
+  __device__ __forceinline__ void ld(uint32_t t) { tc5::tmem_ld32(t, v); }
+};
+template <>
+struct T5Ld<2> {
+  uint32_t v[16];
+  __device__ __forceinline__ void ld(uint32_t t) { tc5::tmem_ld16(t, v); }
+};
+
+struct T5Target {
+  u64 p, np;     // p_j and 2^64 - p_j
+  u32 m;         // floor(2^(sh+32) / p)
+  int sh;        // floor(log2 p) - 32: funnel-shift amount of the quotient window
+  long long off; // element offset of the target row
+};
+// NT targets starting at j0 for this thread's coefficient: orow = out + coefficient,
+// pmk = (p_j - k Q mod p_j) for this coefficient's k (centered; else nullptr).
+// V - qh p lies in [0, 3p) (bconv_tc_kernel's integer quotient), plus p - kQ: [0, 4p);
+// lazy outputs stop there (the forward NTT takes them), else two conditional subtractions.
+template <int NT>
+__device__ __forceinline__ void t5_epilogue(uint32_t taddr, int j0, int nd, const T5Target* tg,
+                                            const u64* pmk, u64* orow, bool lazy) {
+  T5Ld<NT> L;
+  L.ld(taddr);
+  tc5::tmem_wait_ld();
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int j = j0 + u;
+    if (j < nd) {
+      const T5Target T = tg[j];
+      u32 lo, hi, top;
+      tc5::assemble_planes(L.v + 8 * u, lo, hi, top);
+      const u32 qh = __umulhi(__funnelshift_r(hi, top, T.sh), T.m);
+      u64 r = (((u64)hi << 32) | lo) + (u64)qh * T.np;
+      if (pmk) r += pmk[j];
+      if (!lazy) r = csub(csub(r, 2 * T.p), T.p);
+      orow[T.off] = r;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_constant__ BconvGroups G) {
+  pdl_trigger();
+  const BconvArgs& a = G.g[blockIdx.y];
+  extern __shared__ __align__(1024) unsigned char t5sm[];
+  const int nd = a.nd, ns = a.ns;
+  const T5Shape sh = t5_shape(ns, nd);
+  const int kp = sh.kp, nc = sh.nc, ncols = 8 * nc;
+  const int abytes = kT5Rows * kp;                          // one A operand
+  unsigned char* Bm = t5sm + 2 * kT5Groups * abytes;        // B5 chunks
+  T5Target* tg = (T5Target*)(Bm + (size_t)sh.nchunk * ncols * kp);
+  u64* kQs = (u64*)(tg + nd);                               // [ns + 1][nd]: p_j - k Q mod p_j
+  unsigned char* kk = (unsigned char*)(kQs + (a.centered ? nd * (ns + 1) : 0));  // [groups][128]
+  uint64_t* mbar = (uint64_t*)(((uintptr_t)(kk + kT5Groups * kT5Rows) + 7) & ~(uintptr_t)7);
+  uint32_t* tslot = (uint32_t*)(mbar + kT5Groups);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = warp / kT5GW, gw = warp % kT5GW, gtid = tid % (32 * kT5GW);
+  const int quarter = gw & 3, half = gw >> 2;
+  const int n = 1 << a.logn;
+  const int ntiles = n / kT5Rows;
+  const int t0 = blockIdx.x * kT5Tiles;
+  const int t1 = min(t0 + kT5Tiles, ntiles);
+  const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
+  u64* out = a.out + (long long)blockIdx.z * a.out_batch;
+  const unsigned mb_s = tc5::saddr(mbar + grp);
+  unsigned char* abuf = t5sm + grp * 2 * abytes;
+  const unsigned abuf_s = tc5::saddr(abuf);
+  const unsigned b_s = tc5::saddr(Bm);
+  const int bar_id = 1 + grp;
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kT5GW) : "memory"); };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        tc5::saddr(tslot)), "n"(128 * kT5Groups));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (gtid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s));
+  // plan tables (not the predecessor's output): before the PDL wait
+  {
+    const uint4* src = (const uint4*)a.B5;
+    uint4* dst = (uint4*)Bm;
+    for (int i = tid; i < sh.nchunk * ncols * kp / 16; i += blockDim.x) dst[i] = src[i];
+    for (int j = tid; j < nd; j += blockDim.x) {
+      const u64 p = a.pc[a.dst_prime[j]].q;
+      const int s = 63 - __clzll((long long)p);
+      const u32 m = (u32)(((unsigned __int128)1 << (s + 32)) / p);
+      tg[j] = T5Target{p, 0 - p, m, s - 32, a.out_off ? a.out_off[j] : ((long long)j << a.logn)};
+    }
+    if (a.centered)
+      for (int i = tid; i < nd * (ns + 1); i += blockDim.x) {
+        const int j = i / (ns + 1), k = i % (ns + 1);
+        kQs[k * nd + j] = a.pc[a.dst_prime[j]].q - a.kQ[i];
+      }
+    // zero the padding source columns of this group's two A buffers once
+    if (kp > 8 * ns) {
+      const int padw = (kp - 8 * ns) / 8;
+      for (int e = gtid; e < 2 * kT5Rows * padw; e += 32 * kT5GW) {
+        const int bsel = e / (kT5Rows * padw), rem = e % (kT5Rows * padw);
+        const int r = rem % kT5Rows, i = ns + rem / kT5Rows;
+        *(u64*)(abuf + bsel * abytes + tc5::kmaj_off(r, 8 * i, kp)) = 0;
+      }
+    }
+  }
+  // tile staging: 128 coefficients x ns sources, 8-byte cp.async straight into operand
+  // layout.  Thread -> coefficient r = gtid % 128 and sources i = gtid / 128 + 2 k: the
+  // destination advances by one 128-byte core matrix per k, the source by 2 N elements.
+  const int st_r = gtid & (kT5Rows - 1), st_i0 = gtid >> 7;
+  const unsigned st_dst0 = tc5::kmaj_off(st_r, 8 * st_i0, kp);
+  const u64* st_src0 = in + ((long long)st_i0 << a.logn) + st_r;
+  const int st_n = (ns - st_i0 + 1) >> 1;
+  const long long st_step = 2ll << a.logn;
+  auto stage = [&](int tile, int bsel) {
+    unsigned dst = abuf_s + bsel * abytes + st_dst0;
+    const u64* src = st_src0 + (long long)tile * kT5Rows;
+#pragma unroll 1
+    for (int k = 0; k < st_n; ++k, dst += 128, src += st_step)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  pdl_wait();  // the sources are the predecessor's output
+  if (t0 + grp < t1) stage(t0 + grp, 0);
+  tc5::fence_before();
+  __syncthreads();
+  tc5::fence_after();
+  const uint32_t tacc = *tslot + grp * 128;
+  const uint32_t tl = tacc + ((uint32_t)(quarter * 32) << 16);
+  const int m = quarter * 32 + lane;          // this thread's coefficient within the tile
+  const uint32_t idesc = tc5::idesc_i8(ncols);
+  unsigned phase = 0;
+  const bool lazy = a.lazy_out != 0;
+
+  for (int it = 0; t0 + grp + kT5Groups * it < t1; ++it) {
+    const int tile = t0 + grp + kT5Groups * it;
+    unsigned char* A = abuf + (it & 1) * abytes;
+    const unsigned a_s = abuf_s + (it & 1) * abytes;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    gsync();  // the tile is complete (every thread's copies), the other buffer is free
+    if (tile + kT5Groups < t1) stage(tile + kT5Groups, (it + 1) & 1);
+    if (a.src_scale) {
+      for (int e = gtid; e < kT5Rows * ns; e += 32 * kT5GW) {
+        const int i = e / kT5Rows, r = e % kT5Rows;
+        const ulonglong2 sc = a.src_scale[i];
+        u64* px = (u64*)(A + tc5::kmaj_off(r, 8 * i, kp));
+        *px = shoup(*px, sc.x, sc.y, a.pc[a.src_prime[i]].q);
+      }
+      gsync();
+    }
+    if (a.centered) {
+      // k = rint(sum_i fl(v_i) w_i) in the reference's op order (rnspoly.py:320-325)
+      if (gtid < kT5Rows) {
+        double est = 0.0;
+        for (int i = 0; i < ns; ++i)
+          est = __dadd_rn(est, __dmul_rn(__ull2double_rn(*(const u64*)(A + tc5::kmaj_off(gtid, 8 * i, kp))), a.w[i]));
+        kk[grp * kT5Rows + gtid] = (unsigned char)rint(est);
+      }
+    }
+    tc5::fence_async_smem();
+    tc5::fence_before();
+    gsync();
+    tc5::fence_after();
+    u64* orow = out + (long long)tile * kT5Rows + m;
+    const u64* pmk = a.centered ? kQs + (int)kk[grp * kT5Rows + m] * nd : nullptr;
+    for (int c = 0; c < sh.nchunk; ++c) {
+      if (gtid == 0) {
+        for (int s = 0; s < kp / 32; ++s)
+          tc5::mma_i8(tacc, tc5::smem_desc(a_s + s * 256, kp),
+                      tc5::smem_desc(b_s + c * ncols * kp + s * 256, kp), idesc, s > 0);
+        tc5::mma_commit(mb_s);
+      }
+      tc5::mbar_wait(mb_s, phase);
+      phase ^= 1;
+      tc5::fence_after();
+      // this warp's targets of the chunk: [half * nc/2 ...) in steps of 4 / 2
+      const int jh = nc / 2;                       // targets per half (nc even)
+      const int jb = c * nc + half * jh;           // first global target
+      const uint32_t tcol = tl + half * jh * 8;
+      int u = 0;
+#pragma unroll 1
+      for (; u + 4 <= jh; u += 4) t5_epilogue<4>(tcol + 8 * u, jb + u, nd, tg, pmk, orow, lazy);
+      if (u < jh) t5_epilogue<2>(tcol + 8 * u, jb + u, nd, tg, pmk, orow, lazy);  // nc % 4 == 0: jh is even
+      tc5::fence_before();
+      gsync();  // every warp has read D before the next MMA rewrites it
+      tc5::fence_after();
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc5::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(128 * kT5Groups));
+  }
+}
+
+static size_t t5_smem(const BconvArgs& a) {
+  const T5Shape s = t5_shape(a.ns, a.nd);
+  return (size_t)2 * kT5Groups * kT5Rows * s.kp + (size_t)s.nchunk * 8 * s.nc * s.kp +
+         (size_t)a.nd * sizeof(T5Target) + (a.centered ? (size_t)a.nd * (a.ns + 1) * 8 : 0) +
+         kT5Groups * kT5Rows + 8 + kT5Groups * 8 + 16;
+}
+static bool t5_ok(const BconvArgs& a) {
+  return a.B5 != nullptr && a.in_off == nullptr && a.logn >= 7 && a.ns <= 16 && a.nd <= 64 &&
+         t5_smem(a) <= 200 * 1024;
+}
+static void launch_t5(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
+  const int n = 1 << G.g[0].logn;
+  const int tiles = n / kT5Rows;
+  size_t smem = 0;
+  for (int i = 0; i < ng; ++i) smem = std::max(smem, t5_smem(G.g[i]));
+  static unsigned done = 0;  // per-device shared-memory opt-in
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !((done >> dev) & 1u)) {
+    cudaFuncSetAttribute(bconv_t5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);
+  }
+  const dim3 grid((tiles + kT5Tiles - 1) / kT5Tiles, ng, batch);
+  launch_pdl(bconv_t5_kernel, grid, dim3(kT5Threads), smem, st, G);
+}
+
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st) {
   if (ng <= 0 || batch <= 0) return 0;
   if (ng > kMaxBcGroups) return CK_ERR_ARG;
@@ -372,6 +654,12 @@ int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st)
     tc = tc && gs[i].Bf != nullptr && gs[i].c3248 != nullptr && gs[i].tc_ks >= 1 &&
          gs[i].tc_ks <= 4 && gs[i].ns <= 4 * gs[i].tc_ks && gs[i].nd <= 64;
     tks = gs[i].tc_ks > tks ? gs[i].tc_ks : tks;
+  }
+  bool t5 = tc;
+  for (int i = 0; i < ng; ++i) t5 = t5 && t5_ok(gs[i]);
+  if (t5) {
+    launch_t5(G, ng, batch, st);
+    return (int)cudaGetLastError();
   }
   if (tc) {
     if (tks <= 1) launch_tc<1>(G, ng, batch, st);

@@ -166,6 +166,7 @@ struct ck_bconv {
   ulonglong2* d_ihat = nullptr;   // plain ihat (generic apply)
   uint4* d_T = nullptr;
   uint2* d_Bf = nullptr;          // tensor-core B fragments (bconv_tc_kernel)
+  unsigned char* d_B5 = nullptr;  // tcgen05 B chunks (bconv_t5_kernel)
   ulonglong2* d_c3248 = nullptr;
   int tc_ks = 0;
   double* d_w = nullptr;
@@ -214,7 +215,7 @@ struct ck_plan {
   int md_group = 4;   // md_row items per CTA (CKB200_MD_G)
   int bsgs_fused = 1; // fused baby KSKIP + diagonal MAC (CKB200_BSGS_FUSED=0: two kernels)
   int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
-  int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the INT8 tensor-core form
+  int bc_tc = 2;      // CKB200_BCTC=0: CUDA-core base conversion; 1: mma.sync tensor-core form; 2: tcgen05 form
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
   ulonglong2* d_tcD = nullptr;
   std::vector<u64> mod, psi;
@@ -356,6 +357,11 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
             p->mod[dst[j]] > ((u64)1 << 40);
     b->tc_ks = big ? ks : 0;
     b->d_Bf = upload(b->allocs, Bf, err);
+    if (ns >= 1 && ns <= 16 && nd >= 1 && nd <= 64) {
+      std::vector<unsigned char> B5(ck::bconv_t5_table_bytes(ns, nd));
+      ck::bconv_t5_table(Tp.data(), ns, nd, B5.data());
+      b->d_B5 = upload(b->allocs, B5, err);
+    }
     b->d_c3248 = upload(b->allocs, c3248, err);
   }
   b->d_src = upload(b->allocs, src, err);
@@ -515,8 +521,10 @@ int ntt_phase(const ck_plan* p, u64* base, const int* prime, const long long* of
   return ck::launch_ntt_phase(a, jobs, batch, inv, phase, st);
 }
 
+// lazy: a forward NTT consumes the outputs (it takes values below 4p; only the tcgen05
+// kernel uses the flag, every other path writes canonical residues)
 ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
-                         u64* out, long long out_batch, bool prescale) {
+                         u64* out, long long out_batch, bool prescale, bool lazy = false) {
   ck::BconvArgs a;
   a.in = in;
   a.in_batch = in_batch;
@@ -535,16 +543,19 @@ ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, lo
   a.Bf = tc ? bc->d_Bf : nullptr;
   a.c3248 = tc ? bc->d_c3248 : nullptr;
   a.tc_ks = bc->tc_ks;
+  a.B5 = tc && p->bc_tc >= 2 ? bc->d_B5 : nullptr;
   a.ns = bc->ns;
   a.nd = bc->nd;
   a.logn = p->logn;
   a.centered = bc->centered;
+  a.lazy_out = lazy ? 1 : 0;
   return a;
 }
 
 int bconv_run(const ck_plan* p, const ck_bconv* bc, const u64* in, long long in_batch,
-              u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st) {
-  const ck::BconvArgs a = bconv_args(p, bc, in, in_batch, out, out_batch, prescale);
+              u64* out, long long out_batch, bool prescale, int batch, cudaStream_t st,
+              bool lazy = false) {
+  const ck::BconvArgs a = bconv_args(p, bc, in, in_batch, out, out_batch, prescale, lazy);
   return ck::launch_bconv(a, batch, st);
 }
 
@@ -616,12 +627,12 @@ int modup_impl(const ck_plan* p, int l, const u64* a, u64* digits, u64* tmp, int
     ck::BconvArgs gs[ck::kMaxBcGroups];
     for (int d = 0; d < t.beta; ++d)
       gs[d] = bconv_args(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
-                         false);
+                         false, true);
     CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
   } else {
     for (int d = 0; d < t.beta; ++d)
       CK_TRY(bconv_run(p, t.modup_bc[d], tmp + t.lo[d] * N, l * N, digits + d * t.R * N, dig_b,
-                       false, B, st));
+                       false, B, st, true));
   }
   CK_TRY(ntt_rows(p, digits, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs, B,
                   dig_b, false, st));
@@ -693,7 +704,7 @@ int moddown_core(const ck_plan* p, const ModDownTab& m, u64* x, long long xb, u6
   const long long N = p->n;
   CK_TRY(ntt_rows(p, x, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, B, xb, true, st));
   CK_TRY(bconv_run(p, m.bc, x + (long long)m.drop_row0 * N, xb, conv, (long long)m.keep * N, false,
-                   B, st));
+                   B, st, true));
   return ntt_rows(p, conv, m.d_keep_prime, nullptr, nullptr, m.keep, B, (long long)m.keep * N,
                   false, st);
 }
@@ -712,7 +723,7 @@ int moddown_pairs(const ck_plan* p, const ModDownTab& m, u64* x, long long R, u6
   CK_TRY(ntt_phase(p, x, m.d_drop_prime, m.d_drop_off, m.d_drop_scale, m.ndrop, 2 * B, R * N,
                    true, 0, st));
   const ck::BconvArgs g1 = bconv_args(p, m.bc, x + (long long)m.drop_row0 * N, R * N, conv,
-                                      keep * N, false);
+                                      keep * N, false, true);
   CK_TRY(ck::launch_bconv(g1, 2 * B, st));
   CK_TRY(ntt_phase(p, conv, m.d_keep_prime, nullptr, nullptr, m.keep, 2 * B, keep * N, false, 1,
                    st));
@@ -776,12 +787,12 @@ int keyswitch_fused(const ck_plan* p, int level, const u64* a_src, const u64* b_
     ck::BconvArgs gs[ck::kMaxBcGroups];
     for (int d = 0; d < t.beta; ++d)
       gs[d] = bconv_args(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
-                         false);
+                         false, true);
     CK_TRY(ck::launch_bconv_groups(gs, t.beta, B, st));
   } else {
     for (int d = 0; d < t.beta; ++d)
       CK_TRY(bconv_run(p, t.modup_bc[d], w.tmp + t.lo[d] * N, l * N, w.dig + d * R * N, dig_b,
-                       false, B, st));
+                       false, B, st, true));
   }
   CK_TRY(ntt_phase(p, w.dig, t.d_modup_ntt_prime, t.d_modup_ntt_off, nullptr, t.modup_ntt_jobs,
                      B, dig_b, false, 1, st));

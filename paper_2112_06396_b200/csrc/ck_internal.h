@@ -184,7 +184,9 @@ struct BconvArgs {
   const uint2* Bf;              // [tc_ks][4*ceil(nd/4)][32] mma B fragments of T'_{i,a,j} bytes
   const ulonglong2* c3248;      // [nd][2] Shoup pairs of 2^32 and 2^48 mod p_j
   int tc_ks;                    // k-steps of 32 bytes = ceil(ns/4)
+  const unsigned char* B5;      // tcgen05 form (bconv_t5_kernel): B chunks in operand layout (nullable)
   int ns, nd, logn, centered;
+  int lazy_out;                 // tcgen05 form: outputs may stay in [0, 4 p_j) (a forward NTT follows)
 };
 int launch_bconv(const BconvArgs& a, int batch, cudaStream_t st);
 constexpr int kMaxBcGroups = 8;
@@ -194,6 +196,9 @@ struct BconvGroups {
   BconvArgs g[kMaxBcGroups];
 };
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st);
+// tcgen05 B table (host): Tp[(i*8 + a)*nd + j] = T_ij 2^(8a) mod p_j -> operand-layout chunks
+size_t bconv_t5_table_bytes(int ns, int nd);
+void bconv_t5_table(const u64* Tp, int ns, int nd, unsigned char* B5);
 // Key-switching inner product with a fused eval-domain automorphism.
 struct KskipArgs {
   const u64* digits;            // [beta][R][N] raised-basis eval rows
