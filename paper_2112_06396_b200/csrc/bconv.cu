@@ -377,7 +377,12 @@ static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 // own 128 TMEM columns and mbarrier), sharing B and the per-target constants; a
 // pipeline walks its tiles, the next tile's sources streaming in during the
 // epilogues; the two warps of a TMEM lane quarter split each chunk's targets.
-constexpr int kT5Groups = 4, kT5GW = 8, kT5Threads = 32 * kT5GW * kT5Groups;
+#ifndef CKB200_T5_GW
+#define CKB200_T5_GW 4
+#endif
+// warps per pipeline: 4 (one per TMEM lane quarter, up to 128 registers; measured 10.50 vs 10.68 ms per C3 step against 8 = two per quarter at 64 registers)
+constexpr int kT5Groups = 4, kT5GW = CKB200_T5_GW, kT5Threads = 32 * kT5GW * kT5Groups;
+constexpr int kT5Halves = kT5GW / 4;
 constexpr int kT5Rows = 128;
 #ifndef CKB200_T5_TILES
 #define CKB200_T5_TILES 32
@@ -445,17 +450,15 @@ __device__ __forceinline__ void t5_epilogue(uint32_t taddr, int j0, int nd, cons
   tc5::tmem_wait_ld();
 #pragma unroll
   for (int u = 0; u < NT; ++u) {
-    const int j = j0 + u;
-    if (j < nd) {
-      const T5Target T = tg[j];
-      u32 lo, hi, top;
-      tc5::assemble_planes(L.v + 8 * u, lo, hi, top);
-      const u32 qh = __umulhi(__funnelshift_r(hi, top, T.sh), T.m);
-      u64 r = (((u64)hi << 32) | lo) + (u64)qh * T.np;
-      if (pmk) r += pmk[j];
-      if (!lazy) r = csub(csub(r, 2 * T.p), T.p);
-      orow[T.off] = r;
-    }
+    const int j = min(j0 + u, nd - 1);   // padding targets recompute the last one (not stored)
+    const T5Target T = tg[j];
+    u32 lo, hi, top;
+    tc5::assemble_planes(L.v + 8 * u, lo, hi, top);
+    const u32 qh = __umulhi(__funnelshift_r(hi, top, T.sh), T.m);
+    u64 r = (((u64)hi << 32) | lo) + (u64)qh * T.np;
+    if (pmk) r += pmk[j];
+    if (!lazy) r = csub(csub(r, 2 * T.p), T.p);
+    if (j0 + u < nd) orow[T.off] = r;
   }
 }
 
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = warp / kT5GW, gw = warp % kT5GW, gtid = tid % (32 * kT5GW);
-  const int quarter = gw & 3, half = gw >> 2;
+  const int quarter = gw & 3, half = gw >> 2;  // half < kT5Halves
   const int n = 1 << a.logn;
   const int ntiles = n / kT5Rows;
   const int t0 = blockIdx.x * kT5Tiles;
@@ -525,17 +528,18 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
   // tile staging: 128 coefficients x ns sources, 8-byte cp.async straight into operand
   // layout.  Thread -> coefficient r = gtid % 128 and sources i = gtid / 128 + 2 k: the
   // destination advances by one 128-byte core matrix per k, the source by 2 N elements.
+  constexpr int kIs = kT5Halves;  // sources a thread steps over (threads per pipeline / 128)
   const int st_r = gtid & (kT5Rows - 1), st_i0 = gtid >> 7;
-  const unsigned st_dst0 = tc5::kmaj_off(st_r, 8 * st_i0, kp);
+  const unsigned st_dst0 = tc5::kmaj_off(st_r, 0, kp);
   const u64* st_src0 = in + ((long long)st_i0 << a.logn) + st_r;
-  const int st_n = (ns - st_i0 + 1) >> 1;
-  const long long st_step = 2ll << a.logn;
+  const long long st_step = (long long)kIs << a.logn;
   auto stage = [&](int tile, int bsel) {
-    unsigned dst = abuf_s + bsel * abytes + st_dst0;
+    const unsigned dst = abuf_s + bsel * abytes + st_dst0;
     const u64* src = st_src0 + (long long)tile * kT5Rows;
 #pragma unroll 1
-    for (int k = 0; k < st_n; ++k, dst += 128, src += st_step)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    for (int i = st_i0; i < ns; i += kIs, src += st_step)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + ((i >> 1) << 7) + ((i & 1) << 3)),
+                   "l"(src) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   pdl_wait();  // the sources are the predecessor's output
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
       phase ^= 1;
       tc5::fence_after();
       // this warp's targets of the chunk: [half * nc/2 ...) in steps of 4 / 2
-      const int jh = nc / 2;                       // targets per half (nc even)
+      const int jh = nc / kT5Halves;               // targets per warp (a multiple of 2)
       const int jb = c * nc + half * jh;           // first global target
       const uint32_t tcol = tl + half * jh * 8;
       int u = 0;

@@ -48,7 +48,11 @@ namespace {
 
 constexpr int kTcCols = 8;                   // columns per tile (M = 16 x 8 = 128 rows)
 constexpr int kTcGroups = 4;                 // independent 8-warp pipelines per CTA (share B)
-constexpr int kTcGW = 8;                     // warps per group: 2 per TMEM lane quarter
+#ifndef CKB200_TC_GW
+#define CKB200_TC_GW 8
+#endif
+constexpr int kTcGW = CKB200_TC_GW;          // warps per group: 8 = 2 per TMEM lane quarter (4 = 1 at 128 registers: 10.52 vs 10.47 ms per C3 step)
+constexpr int kTcHalves = kTcGW / 4;
 constexpr int kTcThreads = 32 * kTcGW * kTcGroups;
 #ifndef CKB200_TC_TILES
 #define CKB200_TC_TILES 32
@@ -169,7 +173,7 @@ template <int P2, bool INV>
 __device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int c0, int gw, int lane) {
   const int c = lane & 7, e1 = 4 * (gw & 3) + (lane >> 3);   // gw: warp within the group
 #pragma unroll
-  for (int g1 = 8 * (gw >> 2); g1 < 8 * (gw >> 2) + 8; ++g1) {
+  for (int g1 = (16 / kTcHalves) * (gw >> 2); g1 < (16 / kTcHalves) * ((gw >> 2) + 1); ++g1) {
     const int r = INV ? g1 * 16 + e1 : e1 * 16 + g1;
     const u64* src = base + ((long long)r << P2) + c0 + c;
     const unsigned dst = a_dst + kmaj_off(8 * g1 + c, 8 * e1);
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     {
       const int g1 = m >> 3, c = m & 7;
 #pragma unroll 1
-      for (int h = 2 * half; h < 2 * half + 2; ++h) {   // 4 outputs (32 TMEM columns) per wait
+      for (int h = (4 / kTcHalves) * half; h < (4 / kTcHalves) * (half + 1); ++h) {   // 4 outputs (32 TMEM columns) per wait
         uint32_t sv[32];
         tmem_ld32(tl + h * 32, sv);
         tmem_wait_ld();
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
       const int o1 = m >> 3, c = m & 7;
       u64* col = base + c0 + c;
 #pragma unroll 1
-      for (int h = 2 * half; h < 2 * half + 2; ++h) {
+      for (int h = (4 / kTcHalves) * half; h < (4 / kTcHalves) * (half + 1); ++h) {
         uint32_t sv[32];
         tmem_ld32(tl + h * 32, sv);
         tmem_wait_ld();
