@@ -139,230 +139,18 @@ static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 
 
 // ---------------------------------------------------------------------------
-// Tensor-core form.  The contraction is exact integer arithmetic, so it can
-// run on the INT8 tensor cores (mma.sync m16n8k32 u8.u8.s32; measured
-// 568 T MAC/s on this B200, profiles/r01_mma_microbench.txt) instead of the
-// IMAD pipe that bounds the rest of the key-switch:
+// Tensor-core form (default for rings of at least 128 coefficients).  The contraction
+// is exact integer arithmetic, so it runs byte-sliced on the 5th-generation tensor
+// cores (tcgen05.mma kind::i8, accumulators in TMEM) instead of the IMAD pipe that
+// bounds the rest of the key-switch:
 //   x_i        = sum_a x_ia 2^{8a}                 (little-endian bytes, a < 8)
 //   T'_{iaj}   = T_ij 2^{8a} mod p_j = sum_b T'_{iajb} 2^{8b}
-//   S_jb       = sum_{i,a} x_ia T'_{iajb}          (< 128 * 255^2 < 2^23 for <= 4 k-steps)
+//   S_jb       = sum_{i,a} x_ia T'_{iajb}          (< 128 * 255^2 < 2^23)
 //   y_j       == sum_b S_jb 2^{8b}   (mod p_j)
-// A = [coefficients][(i,a)] is the byte view of the u64 source rows (no
-// repacking: a 32-bit A-fragment register is one half of one u64), B =
-// [(i,a)][(j,b)] is precomputed per plan in fragment order.  The n-tiles are
-// arranged so that lane (gid, tig) ends up holding all eight S_jb of target
-// j = 4g + tig for rows gid and gid + 8.
-// Epilogue per (coefficient, target): V = P0 + P1 2^16 + P2 2^32 + P3 2^48
-// (P_k = S_2k + S_2k+1 2^8 < 2^32, V < 2^80); the quotient round(V / p) comes
-// from the FP64 pipe (magic-number conversions, |error| < 2^-16), the
-// remainder from 64-bit integer wrap-around arithmetic, one conditional add.
-// Requires V / p < 2^31 (the quotient is read from 31 mantissa bits): the plan
-// checks the bound per conversion (any target above ~2^48 qualifies).
-// CTAs loop over kTcTiles row tiles with the next tile's sources staged by
-// cp.async while the current one is on the tensor cores.
-constexpr int kTcWarps = 4;
-constexpr int kTcRows = kTcWarps * 32;  // coefficients per tile (2 m16 blocks per warp)
-constexpr int kTcXs = kTcRows + 8;      // padded u64 row stride of the staged sources
-constexpr int kTcTiles = 4;             // row tiles per CTA
-#ifndef CKB200_BCTC_MINB
-#define CKB200_BCTC_MINB 6                // resident CTAs per SM the registers are sized for (4: -1.2%)
-#endif
-
-__device__ __forceinline__ void mma_u8(int (&c)[4], const u32 (&a)[4], uint2 b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-
-struct TcTarget {
-  u64 p;
-  u32 m;        // floor(2^(sh+32) / p)
-  int sh;       // floor(log2 p)
-  long long off;
-};
-
-template <int KS>
-__device__ __forceinline__ void tc_stage(u64* xs, const BconvArgs& a, const u64* in, int row0,
-                                         int n) {
-  // 4*KS source rows x kTcRows coefficients, 16-byte cp.async chunks
-  constexpr int kChunks = kTcRows / 2;
-  for (int e = threadIdx.x; e < a.ns * kChunks; e += blockDim.x) {
-    const int i = e / kChunks, r = 2 * (e - i * kChunks);
-    u64* dst = xs + i * kTcXs + r;
-    const long long off = a.in_off ? a.in_off[i] : ((long long)i << a.logn);
-    if (row0 + r + 1 < n) {
-      cp_async16(dst, in + off + row0 + r);
-    } else {
-      dst[0] = row0 + r < n ? in[off + row0 + r] : 0;
-      dst[1] = 0;
-    }
-  }
-}
-
-template <int KS>
-__global__ void __launch_bounds__(kTcWarps * 32, CKB200_BCTC_MINB) bconv_tc_kernel(const __grid_constant__ BconvGroups G) {
-  pdl_trigger();
-  const BconvArgs& a = G.g[blockIdx.y];
-  extern __shared__ __align__(16) unsigned char tc_smem[];
-  const int nd = a.nd, ns = a.ns;
-  const int ngrp = (nd + 3) >> 2;
-  const int ntile = ngrp * 4;
-  const int tks = a.tc_ks;
-  u64* xsb = (u64*)tc_smem;                                 // [2][4*KS][kTcXs]
-  uint2* bf = (uint2*)(xsb + 2 * 4 * KS * kTcXs);           // [tks][ntile][32]
-  TcTarget* tg = (TcTarget*)(bf + tks * ntile * 32);        // [nd]
-  u64* kQs = (u64*)(tg + nd);                               // [nd][ns+1] (centered)
-  unsigned char* kk = (unsigned char*)(kQs + (a.centered ? nd * (ns + 1) : 0));  // [kTcRows]
-  const int tid = threadIdx.x;
-  const int n = 1 << a.logn;
-  const int ntiles_all = (n + kTcRows - 1) / kTcRows;
-  const int t0 = blockIdx.x * kTcTiles;
-  const int t1 = min(t0 + kTcTiles, ntiles_all);
-  const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
-
-  // zero the padding source rows of both buffers once; stage tile t0
-  for (int e = tid; e < 2 * (4 * KS - ns) * kTcXs; e += blockDim.x) {
-    const int b = e / ((4 * KS - ns) * kTcXs), rem = e - b * ((4 * KS - ns) * kTcXs);
-    xsb[b * 4 * KS * kTcXs + ns * kTcXs + rem] = 0;
-  }
-  for (int i = tid; i < tks * ntile * 32; i += blockDim.x) bf[i] = a.Bf[i];
-  for (int j = tid; j < nd; j += blockDim.x) {
-    const u64 p = a.pc[a.dst_prime[j]].q;
-    const int sh = 63 - __clzll((long long)p);
-    const u32 m = (u32)(((unsigned __int128)1 << (sh + 32)) / p);
-    tg[j] = TcTarget{p, m, sh, a.out_off ? a.out_off[j] : ((long long)j << a.logn)};
-  }
-  if (a.centered)
-    for (int i = tid; i < nd * (ns + 1); i += blockDim.x) kQs[i] = a.kQ[i];
-  pdl_wait();  // the sources are the predecessor's output
-  tc_stage<KS>(xsb, a, in, t0 * kTcRows, n);
-  cp_async_commit();
-
-  const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
-  u64* out = a.out + (long long)blockIdx.z * a.out_batch;
-  for (int t = t0; t < t1; ++t) {
-    u64* xs = xsb + ((t - t0) & 1) * 4 * KS * kTcXs;
-    if (t + 1 < t1) {
-      tc_stage<KS>(xsb + ((t + 1 - t0) & 1) * 4 * KS * kTcXs, a, in, (t + 1) * kTcRows, n);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (a.src_scale) {
-      for (int e = tid; e < ns * kTcRows; e += blockDim.x) {
-        const int i = e / kTcRows, r = e - i * kTcRows;
-        const ulonglong2 sc = a.src_scale[i];
-        xs[i * kTcXs + r] = shoup(xs[i * kTcXs + r], sc.x, sc.y, a.pc[a.src_prime[i]].q);
-      }
-      __syncthreads();
-    }
-    if (a.centered) {
-      // k = rint(sum_i fl(v_i) w_i) in the reference's op order (rnspoly.py:320-325)
-      for (int r = tid; r < kTcRows; r += blockDim.x) {
-        double est = 0.0;
-        for (int i = 0; i < ns; ++i)
-          est = __dadd_rn(est, __dmul_rn(__ull2double_rn(xs[i * kTcXs + r]), a.w[i]));
-        kk[r] = (unsigned char)rint(est);
-      }
-      __syncthreads();
-    }
-    const u32* xw = (const u32*)xs;
-    u32 af[2][KS][4];
-#pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        const int r = warp * 32 + mb * 16 + gid;
-        const int i0 = 4 * s + (tig >> 1), i1 = i0 + 2, w = tig & 1;
-        af[mb][s][0] = xw[(i0 * kTcXs + r) * 2 + w];
-        af[mb][s][1] = xw[(i0 * kTcXs + r + 8) * 2 + w];
-        af[mb][s][2] = xw[(i1 * kTcXs + r) * 2 + w];
-        af[mb][s][3] = xw[(i1 * kTcXs + r + 8) * 2 + w];
-      }
-    const int row0 = t * kTcRows;
-    for (int g = 0; g < ngrp; ++g) {
-      int acc[2][4][4];
-#pragma unroll
-      for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[mb][u][c] = 0;
-#pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        if (s < tks) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint2 b = bf[(s * ntile + g * 4 + u) * 32 + lane];
-            mma_u8(acc[0][u], af[0][s], b);
-            mma_u8(acc[1][u], af[1][s], b);
-          }
-        }
-      }
-      const int j = g * 4 + tig;
-      if (j < nd) {
-        const TcTarget T = tg[j];
-#pragma unroll
-        for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            // S_b = acc[mb][b >> 1][2h + (b & 1)];  P_k = S_2k + S_2k+1 2^8
-            const u32 P0 = (u32)acc[mb][0][2 * h] + ((u32)acc[mb][0][2 * h + 1] << 8);
-            const u32 P1 = (u32)acc[mb][1][2 * h] + ((u32)acc[mb][1][2 * h + 1] << 8);
-            const u32 P2 = (u32)acc[mb][2][2 * h] + ((u32)acc[mb][2][2 * h + 1] << 8);
-            const u32 P3 = (u32)acc[mb][3][2 * h] + ((u32)acc[mb][3][2 * h + 1] << 8);
-            // V mod 2^64, and an integer quotient: W = floor(V / 2^sh) < 2^32 (V/p < 2^31,
-            // checked at plan time), qh = floor(W m / 2^32) undershoots V/p by less than 3
-            // (dropped low bits of V: < 2^sh/p <= 1; m's floor; qh's floor), so
-            // V - qh p is in [0, 3p): two conditional subtractions give the canonical residue
-            const u64 vlo = (u64)P0 + ((u64)P1 << 16) + ((u64)P2 << 32) + ((u64)P3 << 48);
-            const u64 vhi = ((u64)P3 << 16) + P2 + (P1 >> 16);  // floor(V / 2^32), to within 1
-            const u32 qh = __umulhi((u32)(vhi >> (T.sh - 32)), T.m);
-            u64 r = vlo - (u64)qh * T.p;
-            r = csub(csub(r, 2 * T.p), T.p);
-            const int row = warp * 32 + mb * 16 + h * 8 + gid;
-            if (a.centered) r = submod(r, kQs[j * (ns + 1) + kk[row]], T.p);
-            if (row0 + row < n) out[T.off + row0 + row] = r;
-          }
-      }
-    }
-    __syncthreads();  // xs (and kk) are rewritten by the next iteration's staging
-  }
-}
-
-template <int KS>
-static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
-  const int n = 1 << G.g[0].logn;
-  const int tiles = (n + kTcRows - 1) / kTcRows;
-  const dim3 grid((tiles + kTcTiles - 1) / kTcTiles, ng, batch);
-  size_t smem = 0;
-  for (int i = 0; i < ng; ++i) {
-    const BconvArgs& a = G.g[i];
-    const int ntile = ((a.nd + 3) / 4) * 4;
-    const size_t s = (size_t)2 * 4 * KS * kTcXs * 8 + (size_t)a.tc_ks * ntile * 32 * sizeof(uint2) +
-                     (size_t)a.nd * sizeof(TcTarget) +
-                     (a.centered ? (size_t)a.nd * (a.ns + 1) * 8 : 0) + kTcRows;
-    smem = s > smem ? s : smem;
-  }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(bconv_tc_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(bconv_tc_kernel<KS>, grid, dim3(kTcWarps * 32), smem, st, G);
-}
-
-
-// ---------------------------------------------------------------------------
-// tcgen05 form (default for rings of at least 128 coefficients): the same exact
-// byte-sliced contraction as bconv_tc_kernel, on the 5th-generation tensor cores
-// with the accumulators in TMEM.
+// Epilogue per (coefficient, target): V = sum_b S_jb 2^{8b} < 2^80; an integer quotient
+// W = floor(V / 2^sh) < 2^32 (V/p < 2^31 is checked at plan time), qh = floor(W m / 2^32)
+// with m = floor(2^(sh+32) / p) undershoots V/p by less than 3 (dropped low bits of V:
+// < 2^sh/p <= 1; m's floor; qh's floor), so V - qh p is in [0, 3p).
 //   A = [128 coefficients][Kp bytes]: byte a of source i at k = 8 i + a -- the u64
 //       residues themselves, copied by 8-byte cp.async into the canonical K-major
 //       operand layout (no repacking); Kp = 8 ns rounded up to the 32-byte K step.
@@ -370,13 +158,13 @@ static void launch_tc(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 //       a chunk of NC <= 16 targets (tcgen05.mma M128, N = 8 NC, K32 steps).
 //   D = 128 TMEM lanes (coefficients) x N columns of s32 planes.
 // Epilogue: thread = coefficient (TMEM lane); per target the 8 planes are
-// assembled on the ALU pipe (tc5::assemble_planes), reduced with the integer
-// quotient of bconv_tc_kernel, corrected by k Q (centered), and stored -- a warp
-// writes 256 contiguous bytes of one target row.
-// One CTA per SM = 4 independent 8-warp pipelines (own double-buffered A operand,
+// assembled on the ALU pipe (tc5::assemble_planes), reduced with that integer
+// quotient, corrected by k Q (centered), and stored -- a warp writes 256
+// contiguous bytes of one target row.
+// One CTA per SM = 4 independent 4-warp pipelines (own double-buffered A operand,
 // own 128 TMEM columns and mbarrier), sharing B and the per-target constants; a
 // pipeline walks its tiles, the next tile's sources streaming in during the
-// epilogues; the two warps of a TMEM lane quarter split each chunk's targets.
+// epilogues; warp w of a pipeline owns TMEM lanes 32 w .. 32 w + 31.
 #ifndef CKB200_T5_GW
 #define CKB200_T5_GW 4
 #endif
@@ -440,7 +228,7 @@ struct T5Target {
 };
 // NT targets starting at j0 for this thread's coefficient: orow = out + coefficient,
 // pmk = (p_j - k Q mod p_j) for this coefficient's k (centered; else nullptr).
-// V - qh p lies in [0, 3p) (bconv_tc_kernel's integer quotient), plus p - kQ: [0, 4p);
+// V - qh p lies in [0, 3p) (integer quotient, see above), plus p - kQ: [0, 4p);
 // lazy outputs stop there (the forward NTT takes them), else two conditional subtractions.
 template <int NT>
 __device__ __forceinline__ void t5_epilogue(uint32_t taddr, int j0, int nd, const T5Target* tg,
@@ -652,24 +440,10 @@ int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st)
     ns = gs[i].ns > ns ? gs[i].ns : ns;
   }
   count_launches(1);
-  bool tc = true;
-  int tks = 0;
-  for (int i = 0; i < ng; ++i) {
-    tc = tc && gs[i].Bf != nullptr && gs[i].c3248 != nullptr && gs[i].tc_ks >= 1 &&
-         gs[i].tc_ks <= 4 && gs[i].ns <= 4 * gs[i].tc_ks && gs[i].nd <= 64;
-    tks = gs[i].tc_ks > tks ? gs[i].tc_ks : tks;
-  }
-  bool t5 = tc;
+  bool t5 = true;
   for (int i = 0; i < ng; ++i) t5 = t5 && t5_ok(gs[i]);
   if (t5) {
     launch_t5(G, ng, batch, st);
-    return (int)cudaGetLastError();
-  }
-  if (tc) {
-    if (tks <= 1) launch_tc<1>(G, ng, batch, st);
-    else if (tks <= 2) launch_tc<2>(G, ng, batch, st);
-    else if (tks <= 3) launch_tc<3>(G, ng, batch, st);
-    else launch_tc<4>(G, ng, batch, st);
     return (int)cudaGetLastError();
   }
   // smallest compiled source count >= ns (extra source rows are zero)

@@ -165,10 +165,7 @@ struct ck_bconv {
   int* d_dst = nullptr;
   ulonglong2* d_ihat = nullptr;   // plain ihat (generic apply)
   uint4* d_T = nullptr;
-  uint2* d_Bf = nullptr;          // tensor-core B fragments (bconv_tc_kernel)
-  unsigned char* d_B5 = nullptr;  // tcgen05 B chunks (bconv_t5_kernel)
-  ulonglong2* d_c3248 = nullptr;
-  int tc_ks = 0;
+  unsigned char* d_B5 = nullptr;  // tcgen05 B chunks (bconv_t5_kernel); null: CUDA-core kernel only
   double* d_w = nullptr;
   u64* d_kQ = nullptr;
   long long* d_out_off = nullptr; // optional
@@ -215,7 +212,7 @@ struct ck_plan {
   int md_group = 4;   // md_row items per CTA (CKB200_MD_G)
   int bsgs_fused = 1; // fused baby KSKIP + diagonal MAC (CKB200_BSGS_FUSED=0: two kernels)
   int key_prefetch = 2;    // L2 prefetch of the first 2/8 of each key tile in ks_row (8/8: +4 GB DRAM re-reads; 2 best)
-  int bc_tc = 2;      // CKB200_BCTC=0: CUDA-core base conversion; 1: mma.sync tensor-core form; 2: tcgen05 form
+  int bc_tc = 1;      // CKB200_BCTC=0: CUDA-core base conversion instead of the tcgen05 form
   unsigned char* d_tcB = nullptr;  // tensor-core column-phase tables (ntt_tc.cu; CKB200_NTTTC=0 disables)
   ulonglong2* d_tcD = nullptr;
   std::vector<u64> mod, psi;
@@ -303,11 +300,10 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
     for (size_t k = 0; k < src.size(); ++k) qm = mulmod_h(qm, p->mod[src[k]] % pj, pj);
     for (size_t k = 0; k <= src.size(); ++k) kQ[j * (src.size() + 1) + k] = mulmod_h(k % pj, qm, pj);
   }
-  // tensor-core B matrix: B[(i,a)][(j,b)] = byte b of T_ij 2^{8a} mod p_j, in
-  // mma.m16n8k32 fragment order [k-step][n-tile][lane] (see bconv.cu)
+  // tensor-core B matrix: B[(j,b)][(i,a)] = byte b of T_ij 2^{8a} mod p_j, in tcgen05
+  // operand layout (bconv.cu bconv_t5_table)
   {
     const int ns = (int)src.size(), nd = (int)dst.size();
-    const int ks = (ns + 3) / 4, ntile = ((nd + 3) / 4) * 4;
     std::vector<u64> Tp((size_t)ns * 8 * nd);  // [i][a][j]
     for (int i = 0; i < ns; ++i)
       for (int j = 0; j < nd; ++j) {
@@ -320,49 +316,22 @@ ck_bconv* build_bconv(ck_plan* p, const std::vector<int>& src, const std::vector
           sh = mulmod_h(sh, 256 % pj, pj);
         }
       }
-    auto byte_at = [&](int k, int col_t, int gid) -> u32 {
-      const int i = k / 8, aa = k % 8;
-      const int g = col_t / 4, u = col_t % 4;
-      const int j = 4 * g + (gid >> 1), bb = 2 * u + (gid & 1);
-      if (i >= ns || j >= nd) return 0;
-      return (u32)((Tp[((size_t)i * 8 + aa) * nd + j] >> (8 * bb)) & 0xff);
-    };
-    std::vector<uint2> Bf((size_t)ks * ntile * 32);
-    for (int s = 0; s < ks; ++s)
-      for (int tt = 0; tt < ntile; ++tt)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int gid = lane >> 2, tig = lane & 3;
-          u32 b0 = 0, b1 = 0;
-          for (int e = 0; e < 4; ++e) {
-            b0 |= byte_at(32 * s + 4 * tig + e, tt, gid) << (8 * e);
-            b1 |= byte_at(32 * s + 16 + 4 * tig + e, tt, gid) << (8 * e);
-          }
-          Bf[((size_t)s * ntile + tt) * 32 + lane] = make_uint2(b0, b1);
-        }
-    std::vector<ulonglong2> c3248((size_t)nd * 2);
-    for (int j = 0; j < nd; ++j) {
-      const u64 pj = p->mod[dst[j]];
-      c3248[2 * j] = sh2(((u64)1 << 32) % pj, pj);
-      c3248[2 * j + 1] = sh2(((u64)1 << 48) % pj, pj);
-    }
-    // The epilogue quotient V/p must fit 31 bits: bound V = sum_b S_b 2^8b
-    // with S_b <= 32 ks 255^2 (every k-step byte, padding included) and check
-    // V / p_j + 1 < 2^31 for every target (C3: p > 2^53; C5's 50-bit chain: 2^28.6).
-    const double s_max = 32.0 * ks * 255.0 * 255.0;
+    // The epilogue quotient V/p must fit 31 bits: bound V = sum_b S_b 2^8b with
+    // S_b <= Kp 255^2 (every K byte, padding included) and check V / p_j + 2 < 2^31
+    // for every target (C3: p > 2^53; C5's 50-bit chain: 2^28.6); the quotient
+    // window also shifts by floor(log2 p) - 32 >= 8.
+    const int kp = ((8 * ns + 31) / 32) * 32;
+    const double s_max = (double)kp * 255.0 * 255.0;
     const double v_max = s_max * 257.0 * (1.0 + 65536.0 + 4294967296.0 + 281474976710656.0);
-    bool big = true;
-    // (the epilogue's integer quotient also shifts by floor(log2 p) - 32 >= 0)
+    bool big = ns >= 1 && ns <= 16 && nd >= 1 && nd <= 64;
     for (int j = 0; j < nd; ++j)
       big = big && v_max / (double)p->mod[dst[j]] + 2.0 < 2147483648.0 &&
             p->mod[dst[j]] > ((u64)1 << 40);
-    b->tc_ks = big ? ks : 0;
-    b->d_Bf = upload(b->allocs, Bf, err);
-    if (ns >= 1 && ns <= 16 && nd >= 1 && nd <= 64) {
+    if (big) {
       std::vector<unsigned char> B5(ck::bconv_t5_table_bytes(ns, nd));
       ck::bconv_t5_table(Tp.data(), ns, nd, B5.data());
       b->d_B5 = upload(b->allocs, B5, err);
     }
-    b->d_c3248 = upload(b->allocs, c3248, err);
   }
   b->d_src = upload(b->allocs, src, err);
   b->d_dst = upload(b->allocs, dst, err);
@@ -539,11 +508,7 @@ ck::BconvArgs bconv_args(const ck_plan* p, const ck_bconv* bc, const u64* in, lo
   a.T = bc->d_T;
   a.w = bc->d_w;
   a.kQ = bc->d_kQ;
-  const bool tc = p->bc_tc && bc->tc_ks >= 1 && bc->tc_ks <= 4 && bc->nd <= 64;
-  a.Bf = tc ? bc->d_Bf : nullptr;
-  a.c3248 = tc ? bc->d_c3248 : nullptr;
-  a.tc_ks = bc->tc_ks;
-  a.B5 = tc && p->bc_tc >= 2 ? bc->d_B5 : nullptr;
+  a.B5 = p->bc_tc ? bc->d_B5 : nullptr;
   a.ns = bc->ns;
   a.nd = bc->nd;
   a.logn = p->logn;

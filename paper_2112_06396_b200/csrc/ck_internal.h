@@ -180,11 +180,8 @@ struct BconvArgs {
   const uint4* T;               // [ns*nd] {t0,t1,u0,u1}: T = t0+t1 2^30, T 2^30 mod p = u0+u1 2^30
   const double* w;              // [ns] 1.0/q_i   (centered only)
   const u64* kQ;                // [nd*(ns+1)] k*Q mod p_j  (centered only)
-  // tensor-core form (bconv_tc_kernel; nullable -> CUDA-core kernel):
-  const uint2* Bf;              // [tc_ks][4*ceil(nd/4)][32] mma B fragments of T'_{i,a,j} bytes
-  const ulonglong2* c3248;      // [nd][2] Shoup pairs of 2^32 and 2^48 mod p_j
-  int tc_ks;                    // k-steps of 32 bytes = ceil(ns/4)
-  const unsigned char* B5;      // tcgen05 form (bconv_t5_kernel): B chunks in operand layout (nullable)
+  const unsigned char* B5;      // tensor-core form (bconv_t5_kernel): B chunks in tcgen05 operand
+                                // layout; nullable -> CUDA-core kernel
   int ns, nd, logn, centered;
   int lazy_out;                 // tcgen05 form: outputs may stay in [0, 4 p_j) (a forward NTT follows)
 };

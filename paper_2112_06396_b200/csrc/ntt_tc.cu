@@ -38,6 +38,7 @@
 // every consumer folds either.
 #include "ck_internal.h"
 #include "ntt.cuh"
+#include "tc5.cuh"
 
 #include <cstdlib>
 #include <vector>
@@ -61,55 +62,22 @@ constexpr int kTcTiles = CKB200_TC_TILES;    // tiles per CTA (B loaded once per
 constexpr int kOpBytes = 128 * 128;          // one 128-row operand (A), bytes
 constexpr int kBBytes = 128 * 128;           // one B matrix (N = 128 rows of K = 128 bytes)
 
-// Canonical K-major SWIZZLE_NONE layout of rows of 128 bytes: 8x16-byte core
-// matrices, LBO = 128 B between K chunks, SBO = 1024 B between 8-row groups.
+// operands are rows of 128 bytes in the canonical K-major layout of tc5.cuh
 __host__ __device__ __forceinline__ unsigned kmaj_off(int row, int byte) {
-  return ((((unsigned)row >> 3) * 8u + ((unsigned)byte >> 4)) << 7) + (((unsigned)row & 7u) << 4) +
-         ((unsigned)byte & 15u);
+  return tc5::kmaj_off(row, byte, 128);
 }
-
-__device__ __forceinline__ uint64_t smem_desc(unsigned saddr) {
-  const uint64_t lbo = 128 >> 4, sbo = 1024 >> 4;
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | (lbo << 16) | (sbo << 32) | (1ull << 46);
-}
-
+__device__ __forceinline__ uint64_t smem_desc(unsigned saddr) { return tc5::smem_desc(saddr, 128); }
 // kind::i8, A/B unsigned 8-bit, D s32, K-major A and B, M = 128, N = 128
-constexpr uint32_t kIdesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+  tc5::mma_i8(d_tmem, a, b, tc5::idesc_i8(128), acc);
 }
-
-__device__ __forceinline__ unsigned mbar_addr(const uint64_t* b) {
-  return (unsigned)__cvta_generic_to_shared(b);
-}
-__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ unsigned mbar_addr(const uint64_t* b) { return tc5::saddr(b); }
+using tc5::mbar_wait;
+using tc5::tmem_ld32;
+using tc5::tmem_wait_ld;
+__device__ __forceinline__ void tc_fence_before() { tc5::fence_before(); }
+__device__ __forceinline__ void tc_fence_after() { tc5::fence_after(); }
+using tc5::fence_async_smem;
 
 // V = sum_b S_b 2^8b (S_b < 2^23, V < 2^80) reduced into (0, 4p), p > 2^49.5,
 // integer-only: with vhi = floor(V / 2^32) < 2^49, W = floor(vhi / 2^17) < 2^32
@@ -119,28 +87,12 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // < 0.51; the floor: < 1), so V - qh p + p lands in (0, 4p), computed mod 2^64.
 // One mul.hi replaces the FP64 estimate (whose DADD/DFMA bursts throttled the
 // FP64 pipe in every epilogue); the byte-plane assembly stays on the ALU pipe.
-// The byte-plane assembly is written so that ptxas keeps it on the ALU pipe (the
-// fma-heavy pipe is this kernel's limiter and ptxas otherwise turns shift-adds and
-// register moves into IMADs): planes are below 2^24, so s << 8 is a rotate
-// (funnel shift, never an IMAD), and the 16-bit alignments are rotate + mask.
-__device__ __forceinline__ u32 rotl32(u32 x, int n) {
-  u32 r;
-  asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
-  return r;
-}
+// The byte-plane assembly (tc5::assemble_planes) is written so that ptxas keeps it on
+// the ALU pipe: the fma-heavy pipe is this kernel's limiter and ptxas otherwise turns
+// shift-adds and register moves into IMADs.
 __device__ __forceinline__ u64 reduce_lazy(const uint32_t* s, u64 p, u32 m81) {
-  const u32 P0 = s[0] + rotl32(s[1], 8), P1 = s[2] + rotl32(s[3], 8);
-  const u32 P2 = s[4] + rotl32(s[5], 8), P3 = s[6] + rotl32(s[7], 8);  // < 2^32
-  // V = P0 + P1 2^16 + P2 2^32 + P3 2^48 = lo + hi 2^32 + top 2^64
-  const u32 r1 = rotl32(P1, 16), r3 = rotl32(P3, 16);
-  const u32 a_lo = r1 & 0xffff0000u, a_hi = r1 & 0xffffu;
-  const u32 b_lo = r3 & 0xffff0000u, b_hi = r3 & 0xffffu;
   u32 lo, hi, top;
-  asm("add.cc.u32 %0, %1, %2;" : "=r"(lo) : "r"(P0), "r"(a_lo));
-  asm("addc.cc.u32 %0, %1, %2;" : "=r"(hi) : "r"(P2), "r"(a_hi));
-  asm("addc.u32 %0, %1, 0;" : "=r"(top) : "r"(b_hi));
-  asm("add.cc.u32 %0, %0, %1;" : "+r"(hi) : "r"(b_lo));
-  asm("addc.u32 %0, %0, 0;" : "+r"(top));
+  tc5::assemble_planes(s, lo, hi, top);  // V = lo + hi 2^32 + top 2^64
   // vhi = floor(V / 2^32) = hi + top 2^32 < 2^49, W = floor(vhi / 2^17)
   const u32 qh = __umulhi(__funnelshift_r(hi, top, 17), m81);
   const u64 v = ((u64)hi << 32) | lo;
