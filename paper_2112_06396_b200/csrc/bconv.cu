@@ -175,7 +175,9 @@ constexpr int kT5Rows = 128;
 #ifndef CKB200_T5_TILES
 #define CKB200_T5_TILES 32
 #endif
-constexpr int kT5Tiles = CKB200_T5_TILES;  // tiles per CTA (B and the constants loaded once)
+// tiles per CTA (B and the constants are loaded once per CTA): 32 for large batches, fewer
+// when the launch would otherwise not fill the GPU (a single N = 2^12 key-switch)
+constexpr int kT5Tiles = CKB200_T5_TILES;
 
 struct T5Shape {
   int kp, nc, nchunk;
@@ -270,8 +272,8 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
   const int quarter = gw & 3, half = gw >> 2;  // half < kT5Halves
   const int n = 1 << a.logn;
   const int ntiles = n / kT5Rows;
-  const int t0 = blockIdx.x * kT5Tiles;
-  const int t1 = min(t0 + kT5Tiles, ntiles);
+  const int t0 = blockIdx.x * G.tiles_per_cta;
+  const int t1 = min(t0 + G.tiles_per_cta, ntiles);
   const u64* in = a.in + (long long)blockIdx.z * a.in_batch;
   u64* out = a.out + (long long)blockIdx.z * a.out_batch;
   const unsigned mb_s = tc5::saddr(mbar + grp);
@@ -413,9 +415,21 @@ static bool t5_ok(const BconvArgs& a) {
   return a.B5 != nullptr && a.in_off == nullptr && a.logn >= 7 && a.ns <= 16 && a.nd <= 64 &&
          t5_smem(a) <= 200 * 1024;
 }
-static void launch_t5(const BconvGroups& G, int ng, int batch, cudaStream_t st) {
+static void launch_t5(BconvGroups& G, int ng, int batch, cudaStream_t st) {
   const int n = 1 << G.g[0].logn;
   const int tiles = n / kT5Rows;
+  // at least ~2 CTAs per SM when the work allows, never below one tile per pipeline
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long total = (long long)tiles * ng * batch;
+  int tpc = (int)std::min<long long>(kT5Tiles, std::max<long long>(kT5Groups, total / (2 * sms)));
+  tpc = std::max(kT5Groups, (tpc / kT5Groups) * kT5Groups);
+  G.tiles_per_cta = tpc;
   size_t smem = 0;
   for (int i = 0; i < ng; ++i) smem = std::max(smem, t5_smem(G.g[i]));
   static unsigned done = 0;  // per-device shared-memory opt-in
@@ -425,7 +439,7 @@ static void launch_t5(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
     cudaFuncSetAttribute(bconv_t5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);
   }
-  const dim3 grid((tiles + kT5Tiles - 1) / kT5Tiles, ng, batch);
+  const dim3 grid((tiles + tpc - 1) / tpc, ng, batch);
   launch_pdl(bconv_t5_kernel, grid, dim3(kT5Threads), smem, st, G);
 }
 
@@ -433,6 +447,7 @@ int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st)
   if (ng <= 0 || batch <= 0) return 0;
   if (ng > kMaxBcGroups) return CK_ERR_ARG;
   BconvGroups G;
+  G.tiles_per_cta = 0;
   int ns = 0;
   for (int i = 0; i < ng; ++i) {
     if (gs[i].nd <= 0 || gs[i].ns < 1) return CK_ERR_ARG;

@@ -191,6 +191,7 @@ constexpr int kMaxBcGroups = 8;
 // launch: a grid dimension selects the group.
 struct BconvGroups {
   BconvArgs g[kMaxBcGroups];
+  int tiles_per_cta;            // bconv_t5_kernel: 128-coefficient tiles one CTA walks
 };
 int launch_bconv_groups(const BconvArgs* gs, int ng, int batch, cudaStream_t st);
 // tcgen05 B table (host): Tp[(i*8 + a)*nd + j] = T_ij 2^(8a) mod p_j -> operand-layout chunks

@@ -61,15 +61,22 @@ constexpr int kKsEpc = CKB200_KS_EPC;
 #endif
 template <int P2, int LOGN>
 __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt(u64* srow, int g, int sr, const ulonglong2* tw,
-                                                u64 q, u64 two_q) {
+                                                u64 q, u64 two_q, bool canon) {
   u64 x[kE];
   row_from_smem<P2, 0, false>(x, g, srow);
   row_transform<P2, false, LOGN>(x, g, sr << P2, srow, tw, q, two_q);
-  // the 30-bit-split MAC only needs digits < 2^60: for q < 2^56 the lazy
-  // range [0, 16q) already is; larger (special) primes are reduced
+  // the 30-bit-split MAC only needs digits < 2^61 (three products of a value below 2^61 and a
+  // residue accumulate without overflow, their sum stays below 2^64 2^sh for the Barrett step):
+  // for q < 2^56 the lazy range [0, 16q) already is; larger (special) primes are folded to
+  // [0, 2q), and to [0, q) for callers that need canonical values (md_row's exact epilogue)
   if (q >= (1ull << 56)) {
 #pragma unroll
-    for (int k = 0; k < kE; ++k) x[k] = fwd_final(x[k], q);
+    for (int k = 0; k < kE; ++k) {
+      u64 v = csub(x[k], q << 3);
+      v = csub(v, q << 2);
+      v = csub(v, q << 1);
+      x[k] = canon ? csub(v, q) : v;
+    }
   }
   __syncthreads();
   row_to_smem<P2, RowLast<P2>::value, false>(x, g, srow);
@@ -89,9 +96,10 @@ __device__ CK_KS_DIGIT_INLINE void ks_digit_ntt_small(u64* srow, int g, int sr,
 #define CKB200_SMALLQ 1
 #endif
 template <int P2, int LOGN>
-CK_D void ks_digit_ntt_any(u64* srow, int g, int sr, const ulonglong2* tw, u64 q, u64 two_q) {
+CK_D void ks_digit_ntt_any(u64* srow, int g, int sr, const ulonglong2* tw, u64 q, u64 two_q,
+                           bool canon) {
   if (CKB200_SMALLQ && small_prime(q)) ks_digit_ntt_small<P2, LOGN>(srow, g, sr, tw, q);
-  else ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q);
+  else ks_digit_ntt<P2, LOGN>(srow, g, sr, tw, q, two_q, canon);
 }
 
 // KSKIP output: canonical, or [0, 3q) where the consumer takes lazy values
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       else if (d == 1) cp_async_wait<(BETA >= 2 ? BETA - 2 : 0)>();
       else if (d == 2) cp_async_wait<(BETA >= 3 ? BETA - 3 : 0)>();
       else cp_async_wait<0>();
-      if (!own) ks_digit_ntt_any<P2, LOGN>(srow, g, sr, tw, q, two_q);  // own rows are in place
+      if (!own) ks_digit_ntt_any<P2, LOGN>(srow, g, sr, tw, q, two_q, false);  // own rows are in place
     }
   } else {
 #pragma unroll 1
@@ -386,6 +394,8 @@ template <int P1, int P2, bool LAZY>
 #ifndef CKB200_MD_CALL
 #define CKB200_MD_CALL 1
 #endif
+// (the x operand staged by per-thread cp.async during the row NTT was measured again with
+// the cheaper butterflies: 10.9 vs 10.43 ms per C3 step -- removed)
 __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
   using F = FusedCfg<P2>;
   constexpr int LOGN = P1 + P2;
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
     for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
     row_to_smem<P2, 0, false>(y, g, srow);
   }
-  ks_digit_ntt_any<P2, LOGN>(srow, g, r, tw, q, two_q);  // lazy [0,16q) (small primes [0,64q)); q >= 2^56 canonical
+  ks_digit_ntt_any<P2, LOGN>(srow, g, r, tw, q, two_q, true);  // lazy [0,16q) (small primes [0,64q)); q >= 2^56 canonical
   // LAZY instantiation: every kept prime is below 2^59; otherwise decide per row
   const bool lazy = LAZY || q < ((u64)1 << 59);
   const u64 qoff = CKB200_SMALLQ && small_prime(q) ? q << 6 : q << 4;
@@ -446,8 +456,9 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
     const int c = sub_index<P2, 0, false>(g, k);
-    o[k] = lazy ? shoup(x[c] + qoff - srow[sidx(c)], pinv.x, pinv.y, q)
-                : shoup(submod(x[c], srow[sidx(c)], q), pinv.x, pinv.y, q);
+    const u64 xv = x[c];
+    o[k] = lazy ? shoup(xv + qoff - srow[sidx(c)], pinv.x, pinv.y, q)
+                : shoup(submod(xv, srow[sidx(c)], q), pinv.x, pinv.y, q);
   }
   const u64* addp = w ? a.addend : a.addend_u;
   if (addp) {
