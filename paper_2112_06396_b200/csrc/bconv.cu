@@ -169,7 +169,11 @@ static void launch_ns(const BconvGroups& G, int ng, int batch, cudaStream_t st) 
 #define CKB200_T5_GW 4
 #endif
 // warps per pipeline: 4 (one per TMEM lane quarter, up to 128 registers; measured 10.50 vs 10.68 ms per C3 step against 8 = two per quarter at 64 registers)
-constexpr int kT5Groups = 4, kT5GW = CKB200_T5_GW, kT5Threads = 32 * kT5GW * kT5Groups;
+#ifndef CKB200_T5_GROUPS
+#define CKB200_T5_GROUPS 4
+#endif
+constexpr int kT5Groups = CKB200_T5_GROUPS, kT5GW = CKB200_T5_GW, kT5Threads = 32 * kT5GW * kT5Groups;
+constexpr int kT5ColStride = (512 / kT5Groups) & ~31;  // TMEM columns per pipeline
 constexpr int kT5Halves = kT5GW / 4;
 constexpr int kT5Rows = 128;
 #ifndef CKB200_T5_TILES
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-        tc5::saddr(tslot)), "n"(128 * kT5Groups));
+        tc5::saddr(tslot)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (gtid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb_s));
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
   tc5::fence_before();
   __syncthreads();
   tc5::fence_after();
-  const uint32_t tacc = *tslot + grp * 128;
+  const uint32_t tacc = *tslot + grp * kT5ColStride;
   const uint32_t tl = tacc + ((uint32_t)(quarter * 32) << 16);
   const int m = quarter * 32 + lane;          // this thread's coefficient within the tile
   const uint32_t idesc = tc5::idesc_i8(ncols);
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
   __syncthreads();
   if (warp == 0) {
     tc5::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(128 * kT5Groups));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(512));
   }
 }
 
@@ -413,7 +417,7 @@ static size_t t5_smem(const BconvArgs& a) {
 }
 static bool t5_ok(const BconvArgs& a) {
   return a.B5 != nullptr && a.in_off == nullptr && a.logn >= 7 && a.ns <= 16 && a.nd <= 64 &&
-         t5_smem(a) <= 200 * 1024;
+         8 * t5_shape(a.ns, a.nd).nc <= kT5ColStride && t5_smem(a) <= 200 * 1024;
 }
 static void launch_t5(BconvGroups& G, int ng, int batch, cudaStream_t st) {
   const int n = 1 << G.g[0].logn;

@@ -394,6 +394,8 @@ template <int P1, int P2, bool LAZY>
 #ifndef CKB200_MD_CALL
 #define CKB200_MD_CALL 1
 #endif
+// (also re-measured and rejected: prefetching the x / addend lines before the row NTT,
+// 10.44 vs 10.41 ms)
 // (the x operand staged by per-thread cp.async during the row NTT was measured again with
 // the cheaper butterflies: 10.9 vs 10.43 ms per C3 step -- removed)
 __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
