@@ -35,16 +35,20 @@ struct FusedCfg {
 #define CKB200_KS_EPC 1024
 #endif
 #ifndef CKB200_KS_MINB
-#define CKB200_KS_MINB 5
+#define CKB200_KS_MINB 6
 #endif
 // CKB200_KS_RING = S > 0: the key tiles reach shared memory through a ring of S
 // stages of TMA bulk copies (one stage = one MAC iteration's 2*BETA key segments),
 // the first S issued at kernel start so they land during the digit NTTs
 #ifndef CKB200_KS_RING
-#define CKB200_KS_RING 2
+#define CKB200_KS_RING 1
 #endif
-// ks_row elements per CTA (1024: 64 threads; with the 2-stage key ring 38 KB of SMEM, 5 CTAs/SM;
-// measured against 2048 elements x 4 CTAs, rings of 1-8 stages and 2-5 CTAs/SM: DESIGN section 10)
+#ifndef CKB200_KS_EARLY
+#define CKB200_KS_EARLY 1
+#endif
+// ks_row elements per CTA (1024: 64 threads; with a 1-stage key ring that is refilled as soon
+// as the key words are in registers 32 KB of SMEM, 6 CTAs/SM: 10.35 ms per C3 step against
+// 10.48 for the 2-stage ring at 5 CTAs/SM and 10.65 for 3 stages at 4; DESIGN sections 10-11)
 constexpr int kKsEpc = CKB200_KS_EPC;
 
 // Forward row phase of one digit tile in shared memory (natural order in and
@@ -260,6 +264,16 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
         ya[d] = *(const ulonglong2*)(ring + (sl * 2 * BETA + 2 * d) * SEG + 2 * threadIdx.x);
         yb[d] = *(const ulonglong2*)(ring + (sl * 2 * BETA + 2 * d + 1) * SEG + 2 * threadIdx.x);
       }
+#if CKB200_KS_EARLY
+      // the stage is free as soon as every thread holds its key words in registers: refill it
+      // now, so the copy has this whole iteration (MACs, reductions, stores) to land.  The
+      // barrier alone does not wait for shared-memory loads still in flight, and the bulk
+      // copy writes through the async proxy: the proxy fence orders this thread's reads of
+      // the stage before the refill (without it the copy overtook loads: sporadic mismatches).
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0 && m + NSK < ITER) ring_issue(m + NSK);
+#endif
       const int er = e >> P2, ec = e & (F::S - 1);
       const int rr = blockIdx.x * F::TR + er;
       int sc[2];
@@ -288,8 +302,10 @@ __global__ void __launch_bounds__(FusedCfg<P2, kKsEpc>::NT, CKB200_KS_MINB) ks_r
       u64* uw = ubase + tile0 + e;
       *(ulonglong2*)uw = make_ulonglong2(ks_out(su[0], P, lazy_out), ks_out(su[1], P, lazy_out));
       *(ulonglong2*)(uw + a.v_off) = make_ulonglong2(ks_out(sv[0], P, lazy_out), ks_out(sv[1], P, lazy_out));
+#if !CKB200_KS_EARLY
       __syncthreads();  // every thread is done with slot sl
       if (threadIdx.x == 0 && m + NSK < ITER) ring_issue(m + NSK);
+#endif
     }
   } else if constexpr (BETA > 0) {
     // software-pipelined: the key vectors of iteration m+1 are in flight while

@@ -79,11 +79,18 @@ ntt_col_kernel(NttArgs a) {
 
 // --------------------------------------------------------------- row phase
 // grid = (2^P1 / TR, jobs, batch); block = TR * 2^P2 / kE
+// 128 threads per CTA (8 CTAs/SM for rows up to 256 points): 10.13 vs 10.22 ms per C3 step
+// against 256-thread CTAs.  (A per-row shared-memory cache of the four finest levels'
+// twiddles, filled by cp.async, was measured too: 30 KB per 8 rows halves the occupancy,
+// 10.50 ms -- not kept.)
+#ifndef CKB200_NTT_ROW_THREADS
+#define CKB200_NTT_ROW_THREADS 128
+#endif
 template <int P2>
 struct RowCfg {
   static constexpr int S = 1 << P2;
   static constexpr int G = S / kE;
-  static constexpr int TR = 256 / G > 0 ? 256 / G : 1;
+  static constexpr int TR = CKB200_NTT_ROW_THREADS / G > 0 ? CKB200_NTT_ROW_THREADS / G : 1;
   static constexpr int RS = S + S / 16;  // padded smem row stride
 };
 
@@ -91,7 +98,8 @@ struct RowCfg {
 #define CKB200_SMALLQ 1
 #endif
 template <int P1, int P2, bool INV>
-__global__ void __launch_bounds__(256, P2 <= 8 ? CKB200_NTT_ROW_MINB : CKB200_NTT_MINB)
+__global__ void __launch_bounds__(RowCfg<P2>::TR * RowCfg<P2>::G,
+                                  (P2 <= 8 ? CKB200_NTT_ROW_MINB : CKB200_NTT_MINB) * (256 / CKB200_NTT_ROW_THREADS))
 ntt_row_kernel(NttArgs a) {
   using R = RowCfg<P2>;
   constexpr int NP = Sched<P2>::np;

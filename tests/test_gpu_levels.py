@@ -42,6 +42,24 @@ def test_fused_rotate_below_top_level(logn, L, K, dnum, level):
     assert np.array_equal(to_host(out.b.data), want_b)
 
 
+@pytest.mark.parametrize("level", [23, 17])
+def test_fused_rotate_repeatable(level):
+    """The same single key-switch eight times on a nearly empty GPU: ks_row's key stage is
+    refilled by a TMA bulk copy as soon as the key words are in registers; without the proxy
+    fence before that refill the copy overtook in-flight shared-memory loads and these
+    launches (not the full batches) produced sporadic mismatches."""
+    p = _params(16, 24, 8, 3)
+    a, b, kb, ka = synth.rotation_inputs(p, 77, 0, limbs=level)
+    k = 9
+    want_a, want_b = ckks_np.rotate_galois(p, a, b, kb, ka, pow(5, k, 2 * p.n_ring))
+    ks = ckks.KeySet(p, None, None, rot={-k: ckks.SwitchingKey(p.full_moduli, kb, a=ka)})
+    ct = ckks.Ciphertext(RnsPoly(p.chain[:level], a, "eval"), RnsPoly(p.chain[:level], b, "eval"), 1.0)
+    for _ in range(8):
+        out = ckks.rotate(p, ks, ct, -k)
+        assert np.array_equal(to_host(out.a.data), want_a)
+        assert np.array_equal(to_host(out.b.data), want_b)
+
+
 @pytest.mark.parametrize("batch", [1, 3, 5])
 def test_batched_rotate_distinct_galois_small_ring(batch):
     p = _params(12, 6, 2, 3)
