@@ -31,6 +31,9 @@ struct FusedCfg {
   static constexpr int NT = TR * G;        // EPC / 16 threads
   static constexpr int RS = row_stride<P2>();
 };
+#ifndef CKB200_MD_EPC
+#define CKB200_MD_EPC 2048
+#endif
 #ifndef CKB200_KS_EPC
 #define CKB200_KS_EPC 1024
 #endif
@@ -410,12 +413,15 @@ template <int P1, int P2, bool LAZY>
 #ifndef CKB200_MD_CALL
 #define CKB200_MD_CALL 1
 #endif
+#ifndef CKB200_MD_INLINE_SMALL
+#define CKB200_MD_INLINE_SMALL 1
+#endif
 // (also re-measured and rejected: prefetching the x / addend lines before the row NTT,
 // 10.44 vs 10.41 ms)
 // (the x operand staged by per-thread cp.async during the row NTT was measured again with
 // the cheaper butterflies: 10.9 vs 10.43 ms per C3 step -- removed)
-__global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
-  using F = FusedCfg<P2>;
+__global__ void __launch_bounds__(FusedCfg<P2, CKB200_MD_EPC>::NT, CKB200_MD_MINB) md_row_kernel(MdRowArgs a) {
+  using F = FusedCfg<P2, CKB200_MD_EPC>;
   constexpr int LOGN = P1 + P2;
   __shared__ u64 stage[F::TR * F::RS];
   const int j = blockIdx.z;  // grid (row tile, item group, limb)
@@ -441,18 +447,27 @@ __global__ void __launch_bounds__(FusedCfg<P2>::NT, CKB200_MD_MINB) md_row_kerne
   const u64* conv = a.conv + b * a.conv_batch + ro + (a.pair && w ? a.conv_w : 0);
   const u64* x = a.x + b * a.x_batch + ro + (a.pair && w ? a.x_w : 0);
 #if CKB200_MD_CALL
-  // the row NTT as the shared non-inlined ks_digit_ntt (smaller kernel code:
-  // md_row's fully inlined form is ~54 KB of SASS, above the instruction cache)
+  // Small primes (every chain prime of C3/C5): the row NTT inline, straight from the
+  // registers the converted row was loaded into.  Larger primes: the shared non-inlined
+  // ks_digit_ntt (both forms inlined are ~54 KB of SASS, above the instruction cache; a
+  // launch only ever executes one of them per row).
+  const bool small = CKB200_SMALLQ && small_prime(q);
   {
     u64 y[kE];
 #pragma unroll
     for (int k = 0; k < kE; ++k) y[k] = conv[sub_index<P2, 0, false>(g, k)];
-    row_to_smem<P2, 0, false>(y, g, srow);
+    if (CKB200_MD_INLINE_SMALL && small) {
+      row_transform<P2, false, LOGN, SyncCta, true>(y, g, r << P2, srow, tw, neg_opaque(q), q << 2);
+      __syncthreads();
+      row_to_smem<P2, RowLast<P2>::value, false>(y, g, srow);
+    } else {
+      row_to_smem<P2, 0, false>(y, g, srow);
+      ks_digit_ntt_any<P2, LOGN>(srow, g, r, tw, q, two_q, true);  // lazy [0,16q); q >= 2^56 canonical
+    }
   }
-  ks_digit_ntt_any<P2, LOGN>(srow, g, r, tw, q, two_q, true);  // lazy [0,16q) (small primes [0,64q)); q >= 2^56 canonical
   // LAZY instantiation: every kept prime is below 2^59; otherwise decide per row
   const bool lazy = LAZY || q < ((u64)1 << 59);
-  const u64 qoff = CKB200_SMALLQ && small_prime(q) ? q << 6 : q << 4;
+  const u64 qoff = small ? q << 6 : q << 4;   // small primes leave [0, 64q)
   __syncthreads();
 #else
   u64 y[kE];
@@ -541,7 +556,7 @@ static int launch_ks_row_t(const KsRowArgs& a, int rows, int batch, cudaStream_t
 
 template <int P1, int P2>
 static int launch_md_row_t(const MdRowArgs& a, int rows, int batch, cudaStream_t st) {
-  using F = FusedCfg<P2>;
+  using F = FusedCfg<P2, CKB200_MD_EPC>;
   MdRowArgs g = a;
   g.batch = batch;
   const int items = batch * (a.pair ? 2 : 1);
