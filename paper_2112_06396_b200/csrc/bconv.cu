@@ -339,6 +339,9 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
   };
   pdl_wait();  // the sources are the predecessor's output
   if (t0 + grp < t1) stage(t0 + grp, 0);
+  // every thread wrote part of B (and the operand padding) with ordinary stores; the MMAs
+  // read them through the async proxy: fence in the WRITING threads, before the barrier
+  tc5::fence_async_smem();
   tc5::fence_before();
   __syncthreads();
   tc5::fence_after();
