@@ -425,7 +425,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e["matches_device_outputs"] = bool(
             torch.equal(host_out[0], wb.out_a.cpu()) and torch.equal(host_out[1], wb.out_b.cpu()))
         if not args.no_compressed:
-            # compressed keys halve the bytes per unit: bigger chunks pipeline better (measured)
+            # (chunk sizes re-measured with the faster kernels, tools/e2e_sweep.sh: chunks of 4 with
+            # 6 buffers 613, 8/4 599, 16/3 569, 32/2 524 key-switches/s -- the link carries ~60 GB/s
+            # for both directions together, so 4.83 GB in + 1.61 GB out bound it near 600)
             if args.e2e_chunk_compressed != args.e2e_chunk:
                 del pipe
                 pipe = HostRotationPipeline(p, B, chunk=args.e2e_chunk_compressed, nbuf=args.e2e_nbuf)
@@ -773,8 +775,8 @@ def main():
                     help="replay a CUDA-graph capture of one step (non-C3 configs; default: C1 only)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=4)
-    ap.add_argument("--e2e-chunk-compressed", type=int, default=8)
-    ap.add_argument("--e2e-nbuf", type=int, default=4, help="device chunk buffers in the host pipeline")
+    ap.add_argument("--e2e-chunk-compressed", type=int, default=4)
+    ap.add_argument("--e2e-nbuf", type=int, default=6, help="device chunk buffers in the host pipeline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-compressed", action="store_true",
                     help="skip the compressed-key variant of the end-to-end measurement")
