@@ -238,23 +238,28 @@ struct T5Target {
 // V - qh p lies in [0, 3p) (integer quotient, see above), plus p - kQ: [0, 4p);
 // lazy outputs stop there (the forward NTT takes them), else two conditional subtractions.
 template <int NT>
-__device__ __forceinline__ void t5_epilogue(uint32_t taddr, int j0, int nd, const T5Target* tg,
-                                            const u64* pmk, u64* orow, bool lazy) {
-  T5Ld<NT> L;
-  L.ld(taddr);
-  tc5::tmem_wait_ld();
+__device__ __forceinline__ void t5_targets(const uint32_t* v, int j0, int nd, const T5Target* tg,
+                                           const u64* pmk, u64* orow, bool lazy) {
 #pragma unroll
   for (int u = 0; u < NT; ++u) {
     const int j = min(j0 + u, nd - 1);   // padding targets recompute the last one (not stored)
     const T5Target T = tg[j];
     u32 lo, hi, top;
-    tc5::assemble_planes(L.v + 8 * u, lo, hi, top);
+    tc5::assemble_planes(v + 8 * u, lo, hi, top);
     const u32 qh = __umulhi(__funnelshift_r(hi, top, T.sh), T.m);
     u64 r = (((u64)hi << 32) | lo) + (u64)qh * T.np;
     if (pmk) r += pmk[j];
     if (!lazy) r = csub(csub(r, 2 * T.p), T.p);
     if (j0 + u < nd) orow[T.off] = r;
   }
+}
+template <int NT>
+__device__ __forceinline__ void t5_epilogue(uint32_t taddr, int j0, int nd, const T5Target* tg,
+                                            const u64* pmk, u64* orow, bool lazy) {
+  T5Ld<NT> L;
+  L.ld(taddr);
+  tc5::tmem_wait_ld();
+  t5_targets<NT>(L.v, j0, nd, tg, pmk, orow, lazy);
 }
 
 __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_constant__ BconvGroups G) {
@@ -398,6 +403,8 @@ __global__ void __launch_bounds__(kT5Threads, 1) bconv_t5_kernel(const __grid_co
       const int jb = c * nc + half * jh;           // first global target
       const uint32_t tcol = tl + half * jh * 8;
       int u = 0;
+      // (double-buffered TMEM loads, as in the NTT column kernel, were measured here too:
+      // 127 registers, 10.06 vs 9.99 ms per C3 step -- not kept)
 #pragma unroll 1
       for (; u + 4 <= jh; u += 4) t5_epilogue<4>(tcol + 8 * u, jb + u, nd, tg, pmk, orow, lazy);
       if (u < jh) t5_epilogue<2>(tcol + 8 * u, jb + u, nd, tg, pmk, orow, lazy);  // nc % 4 == 0: jh is even

@@ -24,9 +24,9 @@
 // allowed, and the epilogue reduces V = sum_b S_kb 2^8b < 2^80 once (FP64
 // quotient, as in the tensor-core base conversion).
 //
-// Work unit = a tile of 8 columns x 256 rows of one limb; one CTA (1,024
+// Work unit = a tile of 8 columns x 256 rows of one limb; one CTA (512
 // threads, one per SM: 164 KB SMEM, all 512 TMEM columns) runs 4 independent
-// 8-warp pipelines over 32 tiles, sharing B1/B2 and the twists:
+// 4-warp pipelines over 32 tiles, sharing B1/B2 and the twists:
 //   cp.async tile -> A1[(g1,c)][e1]         (128 x 128 B, canonical K-major)
 //   MMA  D1 = A1 . B1^T                     (M128 N128 K128, 128 TMEM columns)
 //   epilogue: y = (V mod p) * twist         -> A2[(o,c)][g1]   (same buffer)
@@ -48,11 +48,17 @@ namespace ck {
 namespace {
 
 constexpr int kTcCols = 8;                   // columns per tile (M = 16 x 8 = 128 rows)
-constexpr int kTcGroups = 4;                 // independent 8-warp pipelines per CTA (share B)
+constexpr int kTcGroups = 4;                 // independent pipelines per CTA (share B)
 #ifndef CKB200_TC_GW
-#define CKB200_TC_GW 8
+#define CKB200_TC_GW 4
 #endif
-constexpr int kTcGW = CKB200_TC_GW;          // warps per group: 8 = 2 per TMEM lane quarter (4 = 1 at 128 registers: 10.52 vs 10.47 ms per C3 step)
+#ifndef CKB200_TC_DB
+#define CKB200_TC_DB 1
+#endif
+constexpr int kTcGW = CKB200_TC_GW;          // warps per group: 4 = one per TMEM lane quarter at up to 128 registers, with
+                                             // double-buffered TMEM loads (CKB200_TC_DB): 10.06 ms per C3 step against 10.13 for
+                                             // 8 warps (two per quarter, 64 registers, one load in flight); 4 warps without the
+                                             // double buffer 10.17
 constexpr int kTcHalves = kTcGW / 4;
 constexpr int kTcThreads = 32 * kTcGW * kTcGroups;
 #ifndef CKB200_TC_TILES
@@ -134,12 +140,13 @@ __device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int 
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Four 8-warp groups per CTA (one CTA per SM: 512 TMEM columns, 32 warps)
+// Four warp groups per CTA (one CTA per SM: 512 TMEM columns)
 // run independent tile pipelines (own double-buffered A operand, TMEM
 // accumulator, mbarrier and named barrier) over tiles g, g+4, ...,
 // sharing the CTA's B matrices and twists.  Tile t+4's data streams in
-// (cp.async) while tile t is on the tensor cores and in the epilogues; the
-// two warps of a TMEM lane quarter split each epilogue's 16 outputs.
+// (cp.async) while tile t is on the tensor cores and in the epilogues; a warp
+// owns one TMEM lane quarter and keeps the next 32 accumulator columns in
+// flight (tcgen05.ld) while it reduces the current ones.
 template <int P2, bool INV>
 __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -221,8 +228,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     tc_fence_after();
     {
       const int g1 = m >> 3, c = m & 7;
+      constexpr int NH = 4 / kTcHalves;               // TMEM loads of 4 outputs (32 columns) each
+      const int h0 = NH * half;
+      if constexpr (CKB200_TC_DB) {
+        // double-buffered TMEM loads: the next 32 columns are in flight while these are reduced
+        uint32_t sv[2][32];
+        tmem_ld32(tl + h0 * 32, sv[0]);
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          tmem_wait_ld();
+          if (hh + 1 < NH) tmem_ld32(tl + (h0 + hh + 1) * 32, sv[(hh + 1) & 1]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int o = (h0 + hh) * 4 + u;
+            const u64 y = reduce_lazy(sv[hh & 1] + 8 * u, p, m81);
+            const ulonglong2 d = tw[o * 16 + g1];
+            st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, np));  // [0, 4p)
+          }
+        }
+      } else {
 #pragma unroll 1
-      for (int h = (4 / kTcHalves) * half; h < (4 / kTcHalves) * (half + 1); ++h) {   // 4 outputs (32 TMEM columns) per wait
+      for (int h = h0; h < h0 + NH; ++h) {   // 4 outputs (32 TMEM columns) per wait
         uint32_t sv[32];
         tmem_ld32(tl + h * 32, sv);
         tmem_wait_ld();
@@ -233,6 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
           const ulonglong2 d = tw[o * 16 + g1];
           st_u64(A, o * 8 + c, g1, shoup_tc(y, d.x, d.y, np));  // [0, 4p)
         }
+      }
       }
     }
     fence_async_smem();
@@ -253,11 +280,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     {
       const int o1 = m >> 3, c = m & 7;
       u64* col = base + c0 + c;
-#pragma unroll 1
-      for (int h = (4 / kTcHalves) * half; h < (4 / kTcHalves) * (half + 1); ++h) {
-        uint32_t sv[32];
-        tmem_ld32(tl + h * 32, sv);
-        tmem_wait_ld();
+      constexpr int NH = 4 / kTcHalves;
+      const int h0 = NH * half;
+      auto out2 = [&](const uint32_t* sv, int h) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int o2 = h * 4 + u;
@@ -266,6 +291,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
             col[(long long)(o2 * 16 + o1) << P2] = csub(csub(shoup_tc(v, scl.x, scl.y, np), 2 * p), p);
           else      // rows 16 o1 + o2; lazy (0, 4p)
             col[(long long)(o1 * 16 + o2) << P2] = v;
+        }
+      };
+      if constexpr (CKB200_TC_DB) {
+        uint32_t sv[2][32];
+        tmem_ld32(tl + h0 * 32, sv[0]);
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          tmem_wait_ld();
+          if (hh + 1 < NH) tmem_ld32(tl + (h0 + hh + 1) * 32, sv[(hh + 1) & 1]);
+          out2(sv[hh & 1], h0 + hh);
+        }
+      } else {
+#pragma unroll 1
+        for (int h = h0; h < h0 + NH; ++h) {
+          uint32_t sv[32];
+          tmem_ld32(tl + h * 32, sv);
+          tmem_wait_ld();
+          out2(sv, h);
         }
       }
     }
