@@ -147,7 +147,7 @@ __device__ __forceinline__ void stage_tile(unsigned a_dst, const u64* base, int 
 // (cp.async) while tile t is on the tensor cores and in the epilogues; a warp
 // owns one TMEM lane quarter and keeps the next 32 accumulator columns in
 // flight (tcgen05.ld) while it reduces the current ones.
-template <int P2, bool INV>
+template <int P2, bool INV, int TILES = kTcTiles>
 __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   unsigned char* Bm = tsm + 2 * kTcGroups * kOpBytes;      // A[group][2] (16 KB each), then B1 | B2
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   const unsigned abuf_s = (unsigned)__cvta_generic_to_shared(tsm) + grp * 2 * kOpBytes;
   unsigned char* abuf = tsm + grp * 2 * kOpBytes;
   const unsigned b_s = (unsigned)__cvta_generic_to_shared(Bm);
-  const int cbase = blockIdx.x * kTcTiles * kTcCols;
+  const int cbase = blockIdx.x * TILES * kTcCols;
   const int bar_id = 1 + grp;
   auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(32 * kTcGW) : "memory"); };
 
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
   const int m = quarter * 32 + lane;                            // this thread's D row
   unsigned phase = 0;
 
-  for (int it = 0; grp + kTcGroups * it < kTcTiles; ++it) {
+  for (int it = 0; grp + kTcGroups * it < TILES; ++it) {
     const int tile = grp + kTcGroups * it;
     const int c0 = cbase + tile * kTcCols;
     unsigned char* A = abuf + (it & 1) * kOpBytes;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
     tc_fence_before();
     gsync();
     tc_fence_after();
-    if (tile + kTcGroups < kTcTiles)
+    if (tile + kTcGroups < TILES)
       stage_tile<P2, INV>(abuf_s + ((it + 1) & 1) * kOpBytes, base, c0 + kTcGroups * kTcCols, gw, lane);
     // ---- pass 1: D1[(r_lo,c)][(beta,b)] = A1 . B1^T
     if (gtid == 0) {
@@ -323,20 +323,42 @@ __global__ void __launch_bounds__(kTcThreads, 1) ntt_col_tc_kernel(NttArgs a) {
 
 constexpr size_t kTcSmem = 2 * kTcGroups * kOpBytes + 2 * kBBytes + 256 * sizeof(ulonglong2) + 72;
 
-template <int P2, bool INV>
-int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
+template <int P2, bool INV, int TILES>
+int launch_tt(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
   // the shared-memory opt-in is per device: track it per device ordinal
   static unsigned done = 0;  // bit d: set on device d (ordinals < 32)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 32 || !((done >> dev) & 1u)) {
-    cudaFuncSetAttribute(ntt_col_tc_kernel<P2, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kTcSmem);
+    cudaFuncSetAttribute(ntt_col_tc_kernel<P2, INV, TILES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
     if (dev < 32) __atomic_fetch_or(&done, 1u << dev, __ATOMIC_RELAXED);
   }
-  const dim3 grid((1 << P2) / (kTcCols * kTcTiles), jobs, batch);
-  launch_pdl(ntt_col_tc_kernel<P2, INV>, grid, dim3(kTcThreads), kTcSmem, st, a);
+  const dim3 grid((1 << P2) / (kTcCols * TILES), jobs, batch);
+  launch_pdl(ntt_col_tc_kernel<P2, INV, TILES>, grid, dim3(kTcThreads), kTcSmem, st, a);
   return 0;
+}
+
+// Tiles per CTA: kTcTiles (one table load and TMEM allocation per 32 column tiles) when that
+// still gives every SM several CTAs; a quarter of that for small batches (one ciphertext:
+// 16-72 limb jobs), so the launch spreads over the GPU instead of over jobs x batch SMs.
+// CKB200_TC_SPLIT=0/1 forces the choice (measurements).
+template <int P2, bool INV>
+int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
+  static const int force = [] {
+    const char* e = getenv("CKB200_TC_SPLIT");
+    return e ? atoi(e) : -1;
+  }();
+  static const int sms = [] {
+    int d = 0, n = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
+  const long long ctas = (long long)((1 << P2) / (kTcCols * kTcTiles)) * jobs * batch;
+  const bool split = force >= 0 ? force != 0 : ctas < 4LL * sms;
+  return split ? launch_tt<P2, INV, kTcTiles / 4>(a, jobs, batch, st)
+               : launch_tt<P2, INV, kTcTiles>(a, jobs, batch, st);
 }
 
 // ---------------------------------------------------------------- host side
