@@ -19,6 +19,7 @@
 // per accumulator) accumulate without overflow; more sources are chunked.
 // The float estimate replicates numpy's op order with explicit _rn
 // intrinsics (no FMA contraction), round-half-even via rint().
+#include <cstdlib>
 #include "ck_internal.h"
 #include "tc5.cuh"
 
@@ -444,6 +445,25 @@ static void launch_t5(BconvGroups& G, int ng, int batch, cudaStream_t st) {
   const long long total = (long long)tiles * ng * batch;
   int tpc = (int)std::min<long long>(kT5Tiles, std::max<long long>(kT5Groups, total / (2 * sms)));
   tpc = std::max(kT5Groups, (tpc / kT5Groups) * kT5Groups);
+  // Small launches (one ciphertext, hoisted batches of a few): the kernel runs ONE CTA per SM
+  // (TMEM and shared memory), so the grid is sized in whole waves -- pick the tiles per CTA
+  // that minimise waves x (prologue + iterations), a CTA's prologue (TMEM allocation, B table)
+  // costing about two tile iterations.  CKB200_T5_WAVES=0 keeps the plain rule (measurements).
+  static const int wave_rule = [] {
+    const char* e = getenv("CKB200_T5_WAVES");
+    return e ? atoi(e) : 1;
+  }();
+  if (wave_rule && total < 4LL * kT5Tiles * sms) {
+    long long best = -1;
+    for (int c = kT5Groups; c <= kT5Tiles; c += kT5Groups) {
+      const long long ctas = (long long)((tiles + c - 1) / c) * ng * batch;
+      const long long cost = ((ctas + sms - 1) / sms) * (2 + c / kT5Groups);
+      if (best < 0 || cost < best) {
+        best = cost;
+        tpc = c;
+      }
+    }
+  }
   G.tiles_per_cta = tpc;
   size_t smem = 0;
   for (int i = 0; i < ng; ++i) smem = std::max(smem, t5_smem(G.g[i]));
