@@ -339,26 +339,45 @@ int launch_tt(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
   return 0;
 }
 
-// Tiles per CTA: kTcTiles (one table load and TMEM allocation per 32 column tiles) when that
-// still gives every SM several CTAs; a quarter of that for small batches (one ciphertext:
-// 16-72 limb jobs), so the launch spreads over the GPU instead of over jobs x batch SMs.
-// CKB200_TC_SPLIT=0/1 forces the choice (measurements).
+// Tiles per CTA.  The kernel runs ONE CTA per SM (TMEM, shared memory), so a launch takes
+// whole waves: kTcTiles = 32 (one table load and TMEM allocation per 32 column tiles) for
+// large batches; for small launches (one ciphertext: 16-72 limb jobs; hoisted batches of a
+// few) the count among 8 / 16 / 32 that minimises waves x (prologue + iterations), a CTA's
+// prologue costing about two iterations of its four pipelines.
+// CKB200_TC_SPLIT = 8 / 16 / 32 forces the count (0 / 1: 32 / 8) (measurements, tests).
 template <int P2, bool INV>
 int launch_t(const NttArgs& a, int jobs, int batch, cudaStream_t st) {
   static const int force = [] {
     const char* e = getenv("CKB200_TC_SPLIT");
-    return e ? atoi(e) : -1;
+    const int v = e ? atoi(e) : -1;
+    return v == 0 ? 32 : v == 1 ? 8 : v;
   }();
   static const int sms = [] {
     int d = 0, n = 148;
     cudaGetDevice(&d);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-    return n;
+    return n > 0 ? n : 148;
   }();
-  const long long ctas = (long long)((1 << P2) / (kTcCols * kTcTiles)) * jobs * batch;
-  const bool split = force >= 0 ? force != 0 : ctas < 4LL * sms;
-  return split ? launch_tt<P2, INV, kTcTiles / 4>(a, jobs, batch, st)
-               : launch_tt<P2, INV, kTcTiles>(a, jobs, batch, st);
+  int tiles = kTcTiles;
+  const long long per = (long long)jobs * batch;
+  if (force == 8 || force == 16 || force == 32) {
+    tiles = force;
+  } else if (per * ((1 << P2) / (kTcCols * kTcTiles)) < 8LL * sms) {
+    long long best = -1;
+    for (int c = 8; c <= kTcTiles; c *= 2) {
+      const long long ctas = per * ((1 << P2) / (kTcCols * c));
+      const long long cost = ((ctas + sms - 1) / sms) * (2 + c / kTcGroups);
+      if (best < 0 || cost < best) {
+        best = cost;
+        tiles = c;
+      }
+    }
+  }
+  switch (tiles) {
+    case 8: return launch_tt<P2, INV, 8>(a, jobs, batch, st);
+    case 16: return launch_tt<P2, INV, 16>(a, jobs, batch, st);
+    default: return launch_tt<P2, INV, kTcTiles>(a, jobs, batch, st);
+  }
 }
 
 // ---------------------------------------------------------------- host side

@@ -38,10 +38,11 @@ VARIANTS = {
     "unfused": {"CKB200_UNFUSED": "1"},
     "bc_cuda_cores": {"CKB200_BCTC": "0"},
     "no_programmatic_dependent_launch": {"CKB200_PDL": "0"},
-    # tensor-core column phase: 32 column tiles per CTA (large batches) / 8 (small batches);
-    # the launcher picks by grid size, these force each on the one-ciphertext goldens
-    "col_tiles_32": {"CKB200_TC_SPLIT": "0"},
-    "col_tiles_8": {"CKB200_TC_SPLIT": "1"},
+    # tensor-core column phase: 32 column tiles per CTA (large batches), 16 or 8 (small
+    # launches); the launcher picks by whole waves, these force each on the goldens
+    "col_tiles_32": {"CKB200_TC_SPLIT": "32"},
+    "col_tiles_16": {"CKB200_TC_SPLIT": "16"},
+    "col_tiles_8": {"CKB200_TC_SPLIT": "8"},
 }
 
 
